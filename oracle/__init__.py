@@ -1,0 +1,266 @@
+"""CPU oracle for the Speedy-Splat forward hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / `--impl reference`
+legs may import this package.  The product path (paper_2412_00578_b200) never imports,
+links or executes it; the two share no code.  The arithmetic lives in ss_oracle.c
+(plain C, -ffp-contract=off); this module only marshals numpy arrays through ctypes.
+See ss_oracle.c's header for the precision contract and the citations.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ss_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+
+MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}
+R_NF = 12
+REC_FIELDS = ["x", "y", "depth", "a", "b", "c", "sigma", "t", "r", "g", "b_", "vis"]
+
+GCC_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-Wall", "-shared", "-fPIC"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so (plain C; the checker, not the product)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", *GCC_FLAGS, "-o", _LIB_PATH, _SRC, "-lm"])
+    return _LIB_PATH
+
+
+class OrCamera(C.Structure):
+    _fields_ = [("viewmat", C.c_float * 12), ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float),
+                ("cy", C.c_float), ("campos", C.c_float * 3), ("width", C.c_int32), ("height", C.c_int32),
+                ("z_near", C.c_float), ("clip", C.c_float)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        d, f, i, u32, u64, vp = C.c_double, C.c_float, C.c_int, C.c_uint32, C.c_uint64, C.c_void_p
+        sig = {
+            "or_sh_basis": (None, [i, f, f, f, vp]),
+            "or_threshold": (d, [f]),
+            "or_snugbox": (None, [d, d, d, d, d, d, vp, vp]),
+            "or_rect_snugbox": (None, [d, d, d, d, d, d, i, i, vp]),
+            "or_rect_3sigma": (None, [d, d, d, d, d, i, i, vp]),
+            "or_accutile": (u32, [d, d, d, d, d, d, i, i, vp, u32, vp, i]),
+            "or_tiles_exact": (u32, [d, d, d, d, d, d, i, i, vp]),
+            "or_project": (None, [i, i, vp, vp, vp, vp, vp, i, vp, vp, vp]),
+            "or_tiles_of_record": (u32, [i, vp, vp, i, i, vp, u32]),
+            "or_exclusive_scan": (u64, [i, vp, vp]),
+            "or_duplicate_with_keys": (u64, [i, i, vp, vp, vp, vp, i, i, vp, vp]),
+            "or_sort_pairs": (None, [u64, vp, vp]),
+            "or_tile_ranges": (None, [u64, vp, i, vp]),
+            "or_render": (None, [vp, vp, vp, i, i, vp, vp, vp, vp]),
+            "or_global_order": (None, [i, vp, vp, vp]),
+            "or_render_unbinned": (None, [vp, vp, u32, i, i, vp, i, i, i, i, vp]),
+            "or_prune_score": (None, [vp, vp, vp, i, vp, vp, i, i, i, i]),
+            "or_composite_alphas": (None, [i, vp, vp, vp, vp]),
+            "or_frame": (u64, [i, i, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp, vp, vp, u64, vp, vp, vp, vp]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(_lib, name)
+            fn.restype = res
+            fn.argtypes = args
+    return _lib
+
+
+def _p(a: np.ndarray | None):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "oracle arrays must be C-contiguous"
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def camera(cam) -> OrCamera:
+    oc = OrCamera()
+    oc.viewmat[:] = [float(v) for v in np.asarray(cam.viewmat, np.float32).reshape(-1)]
+    oc.fx, oc.fy, oc.cx, oc.cy = cam.fx, cam.fy, cam.cx, cam.cy
+    oc.campos[:] = [float(v) for v in np.asarray(cam.campos, np.float32)]
+    oc.width, oc.height, oc.z_near, oc.clip = cam.width, cam.height, cam.z_near, cam.clip
+    return oc
+
+
+# ---- geometry -------------------------------------------------------------------------
+
+def sh_basis(deg: int, x: float, y: float, z: float) -> np.ndarray:
+    out = np.zeros(16, np.float32)
+    lib().or_sh_basis(deg, x, y, z, _p(out))
+    return out
+
+
+def threshold(sigma: float) -> float:
+    return lib().or_threshold(sigma)
+
+
+def snugbox(mx, my, a, b, c, t):
+    bb = np.zeros(4)
+    tg = np.zeros(8)
+    lib().or_snugbox(mx, my, a, b, c, t, _p(bb), _p(tg))
+    return bb, tg.reshape(4, 2)
+
+
+def rect_snugbox(mx, my, a, b, c, t, tiles_x, tiles_y):
+    r = np.zeros(4, np.int32)
+    lib().or_rect_snugbox(mx, my, a, b, c, t, tiles_x, tiles_y, _p(r))
+    return tuple(int(v) for v in r)
+
+
+def rect_3sigma(mx, my, cxx, cxy, cyy, tiles_x, tiles_y):
+    r = np.zeros(4, np.int32)
+    lib().or_rect_3sigma(mx, my, cxx, cxy, cyy, tiles_x, tiles_y, _p(r))
+    return tuple(int(v) for v in r)
+
+
+def accutile(mx, my, a, b, c, t, tiles_x, tiles_y, force_dir=-1):
+    """Returns (sorted tile-id array, n_line_solves)."""
+    cap = tiles_x * tiles_y + 1
+    out = np.zeros(cap, np.uint32)
+    ns = C.c_int32(0)
+    n = lib().or_accutile(mx, my, a, b, c, t, tiles_x, tiles_y, _p(out), cap, C.byref(ns), force_dir)
+    return np.sort(out[:n]), ns.value
+
+
+def tiles_exact(mx, my, a, b, c, t, tiles_x, tiles_y) -> np.ndarray:
+    mask = np.zeros(tiles_x * tiles_y, np.uint8)
+    lib().or_tiles_exact(mx, my, a, b, c, t, tiles_x, tiles_y, _p(mask))
+    return np.nonzero(mask)[0].astype(np.uint32)
+
+
+# ---- pipeline -------------------------------------------------------------------------
+
+def project(scene, cam, mode: str):
+    n = scene.n
+    rec = np.zeros((n, R_NF), np.float32)
+    rect = np.zeros((n, 4), np.int32)
+    cnt = np.zeros(n, np.uint32)
+    lib().or_project(n, scene.sh_degree, _p(scene.mean_opac), _p(scene.scale), _p(scene.rot), _p(scene.sh),
+                     C.byref(camera(cam)), MODES[mode], _p(rec), _p(rect), _p(cnt))
+    return rec, rect, cnt
+
+
+def tiles_of_record(mode: str, rec_row: np.ndarray, rect_row: np.ndarray, tiles_x, tiles_y) -> np.ndarray:
+    rec_row = np.ascontiguousarray(rec_row, np.float32)
+    rect_row = np.ascontiguousarray(rect_row, np.int32)
+    cap = tiles_x * tiles_y + 1
+    out = np.zeros(cap, np.uint32)
+    n = lib().or_tiles_of_record(MODES[mode], _p(rec_row), _p(rect_row), tiles_x, tiles_y, _p(out), cap)
+    return out[:n].copy()
+
+
+def exclusive_scan(counts: np.ndarray):
+    counts = np.ascontiguousarray(counts, np.uint32)
+    off = np.zeros(len(counts), np.uint64)
+    total = lib().or_exclusive_scan(len(counts), _p(counts), _p(off))
+    return off, int(total)
+
+
+def sort_pairs(keys: np.ndarray, values: np.ndarray):
+    k = np.ascontiguousarray(keys, np.uint64).copy()
+    v = np.ascontiguousarray(values, np.uint32).copy()
+    lib().or_sort_pairs(len(k), _p(k), _p(v))
+    return k, v
+
+
+def tile_ranges(sorted_keys: np.ndarray, n_tiles: int) -> np.ndarray:
+    k = np.ascontiguousarray(sorted_keys, np.uint64)
+    r = np.zeros((n_tiles, 2), np.uint32)
+    lib().or_tile_ranges(len(k), _p(k), n_tiles, _p(r))
+    return r
+
+
+class Frame:
+    """Every intermediate of one oracle view (CS3)."""
+
+    def __init__(self, **kw):
+        self.__dict__.update(kw)
+
+
+def frame(scene, cam, mode: str = "accutile", bg=(0.0, 0.0, 0.0), render=True) -> Frame:
+    n = scene.n
+    rec = np.zeros((n, R_NF), np.float32)
+    rect = np.zeros((n, 4), np.int32)
+    cnt = np.zeros(n, np.uint32)
+    off = np.zeros(n, np.uint64)
+    n_tiles = cam.tiles_x * cam.tiles_y
+    ranges = np.zeros((n_tiles, 2), np.uint32)
+    bgv = np.asarray(bg, np.float32)
+    oc = camera(cam)
+    cap = 0
+    keys = np.zeros(1, np.uint64)
+    vals = np.zeros(1, np.uint32)
+    img = np.zeros((3, cam.height, cam.width), np.float32) if render else None
+    T = np.zeros((cam.height, cam.width), np.float32) if render else None
+    nc = np.zeros((cam.height, cam.width), np.uint32) if render else None
+    for _ in range(2):
+        P = lib().or_frame(n, scene.sh_degree, _p(scene.mean_opac), _p(scene.scale), _p(scene.rot),
+                           _p(scene.sh), C.byref(oc), MODES[mode], _p(bgv), _p(rec), _p(rect), _p(cnt),
+                           _p(off), _p(keys), _p(vals), cap, _p(ranges), _p(img), _p(T), _p(nc))
+        if P <= cap:
+            break
+        cap = int(P)
+        keys = np.zeros(max(cap, 1), np.uint64)
+        vals = np.zeros(max(cap, 1), np.uint32)
+    P = int(P)
+    return Frame(rec=rec, rect=rect, counts=cnt, offsets=off, P=P, keys=keys[:P], values=vals[:P],
+                 ranges=ranges, image=img, T=T, ncontrib=nc, mode=mode, bg=bgv)
+
+
+def render(rec, values, ranges, width, height, bg=(0.0, 0.0, 0.0)):
+    img = np.zeros((3, height, width), np.float32)
+    T = np.zeros((height, width), np.float32)
+    nc = np.zeros((height, width), np.uint32)
+    bgv = np.asarray(bg, np.float32)
+    lib().or_render(_p(np.ascontiguousarray(rec, np.float32)), _p(np.ascontiguousarray(values, np.uint32)),
+                    _p(np.ascontiguousarray(ranges, np.uint32)), width, height, _p(bgv), _p(img), _p(T), _p(nc))
+    return img, T, nc
+
+
+def render_unbinned(rec, width, height, bg=(0.0, 0.0, 0.0), window=None):
+    rec = np.ascontiguousarray(rec, np.float32)
+    order = np.zeros(len(rec), np.uint32)
+    nv = C.c_uint32(0)
+    lib().or_global_order(len(rec), _p(rec), _p(order), C.byref(nv))
+    img = np.zeros((3, height, width), np.float32)
+    x0, x1, y0, y1 = window if window else (0, width, 0, height)
+    bgv = np.asarray(bg, np.float32)
+    lib().or_render_unbinned(_p(rec), _p(order), nv.value, width, height, _p(bgv), x0, x1, y0, y1, _p(img))
+    return img
+
+
+def prune_score(rec, values, ranges, width, height, bg=(0.0, 0.0, 0.0), score=None, window=None):
+    rec = np.ascontiguousarray(rec, np.float32)
+    if score is None:
+        score = np.zeros(len(rec), np.float64)
+    x0, x1, y0, y1 = window if window else (0, width, 0, height)
+    bgv = np.asarray(bg, np.float32)
+    lib().or_prune_score(_p(rec), _p(np.ascontiguousarray(values, np.uint32)),
+                         _p(np.ascontiguousarray(ranges, np.uint32)), width, _p(bgv), _p(score),
+                         x0, x1, y0, y1)
+    return score
+
+
+def composite_alphas(alpha, rgb, bg=(0.0, 0.0, 0.0)) -> np.ndarray:
+    alpha = np.ascontiguousarray(alpha, np.float64)
+    rgb = np.ascontiguousarray(rgb, np.float64)
+    out = np.zeros(3)
+    lib().or_composite_alphas(len(alpha), _p(alpha), _p(rgb), _p(np.asarray(bg, np.float64)), _p(out))
+    return out
+
+
+def score_views(scene, cams, mode="accutile", bg=(0.0, 0.0, 0.0)) -> np.ndarray:
+    """U~ summed over a list of views (oracle side of the multi-view score)."""
+    s = np.zeros(scene.n, np.float64)
+    for cam in cams:
+        f = frame(scene, cam, mode, bg, render=False)
+        prune_score(f.rec, f.values, f.ranges, cam.width, cam.height, bg, s)
+    return s
