@@ -1,0 +1,192 @@
+/*
+ * ss.h -- C ABI of libss.so, the sm_100a (B200) Speedy-Splat forward hot path.
+ *
+ * One view ("frame") of a 3D Gaussian Splatting scene is rendered by four calls, in
+ * order, on one CUDA stream, followed optionally by the pruning-score call:
+ *
+ *   ss_preprocess  projection + tile count            PAPER.md Sec. 3.2.1
+ *   ss_bin         key allocation + key emission       InclusiveSum / duplicateWithKeys
+ *   ss_sort        sort by (tile, depth) + tile ranges RadixSort / identifyTileRanges
+ *   ss_render      per-tile front-to-back blending     Sec. 3.2.3, Eqs. 5-7
+ *   ss_prune_score efficient pruning score, +=         Sec. 4.2.1, Eqs. 20-21
+ *
+ * The tile test of ss_preprocess / ss_bin is selected by ss_bin_mode: the 3D-GS 3-sigma
+ * square (Eq. 8), SnugBox (Sec. 4.1.1, Eqs. 15-16) or AccuTile
+ * (Sec. 4.1.2, Algorithm 1).
+ *
+ * Conventions (DESIGN.md §2-§3 states every reading of the paper behind them):
+ *   - Every pointer is a DEVICE pointer unless marked (host).  Device buffers are owned by
+ *     the caller; libss never allocates, frees or keeps global state.  All calls enqueue
+ *     work on `stream` (a cudaStream_t passed as void*, NULL = legacy default stream) and
+ *     return without synchronising.  Calls on different streams with disjoint frame
+ *     workspaces may run concurrently.
+ *   - Per-frame intermediates live in ONE caller-allocated device workspace described by
+ *     ss_frame (size from ss_frame_workspace_size, sub-buffer offsets from ss_frame_layout).
+ *     Sizes that only the device knows (visible count, pair count P) stay on the device;
+ *     no call reads them back to the host.
+ *   - Errors: host-side validation happens before any launch and returns
+ *     SS_ERR_INVALID_ARG (null required pointer, n < 0, width/height <= 0, sh_degree not in
+ *     0..3, workspace too small, mode out of range) or SS_ERR_UNSUPPORTED (more than 65536
+ *     tiles, n or capacity >= 2^30).  A failed launch returns SS_ERR_CUDA (the CUDA error
+ *     string is available from ss_last_cuda_error of the same thread).  Device-side faults
+ *     surface on the caller's next synchronisation.  Pair-array overflow is NOT an error
+ *     code: ss_bin writes min(P, capacity) pairs, stores P in the workspace's total_pairs
+ *     and sets its overflow flag; the caller reads them, grows `capacity` and re-runs the
+ *     frame (every call is idempotent given the same inputs).
+ */
+#ifndef SS_H
+#define SS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SS_API __attribute__((visibility("default")))
+#else
+#define SS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SS_OK = 0,
+    SS_ERR_INVALID_ARG = 1,
+    SS_ERR_CAPACITY = 2, /* reserved: capacity overflow is reported through the workspace flag */
+    SS_ERR_CUDA = 3,
+    SS_ERR_UNSUPPORTED = 4
+} ss_status;
+
+typedef enum {
+    SS_BIN_3SIGMA = 0,   /* baseline: tiles meeting the square mu +- ceil(3 sqrt(lambda_max)), Eq. 8 */
+    SS_BIN_SNUGBOX = 1,  /* tiles meeting the exact bbox of the alpha >= 1/255 ellipse, Eqs. 14-16 */
+    SS_BIN_ACCUTILE = 2  /* exactly the tiles meeting that ellipse, Algorithm 1 */
+} ss_bin_mode;
+
+/* Gaussian set G = {mu, s, r, h, sigma} (Eq. 1), SoA float32 planes in HBM.
+ * Parameters are ACTIVATED: linear scales, opacity in (0,1); the quaternion is normalised
+ * in-kernel.  SH coefficient k = basis*3 + channel is component k%4 of plane k/4; plane p
+ * is the float4 array sh + 4*n*p.  Planes: deg 0 -> 1, 1 -> 3, 2 -> 7, 3 -> 12. */
+typedef struct {
+    int32_t n;              /* number of Gaussians, 0 <= n < 2^30                            */
+    int32_t sh_degree;      /* 0..3                                                          */
+    const float *mean_opac; /* [n][4]  x, y, z (world), opacity sigma                         */
+    const float *scale;     /* [n][4]  sx, sy, sz (linear), unused                            */
+    const float *rot;       /* [n][4]  quaternion w, x, y, z                                  */
+    const float *sh;        /* [planes][n][4]                                                 */
+} ss_scene;
+
+/* Pinhole camera (host struct, copied into kernel arguments).  Pixel (col,row) has
+ * coordinate (col,row); x2d = fx * X/Z + cx, y2d = fy * Y/Z + cy in camera space
+ * p = viewmat[:, :3] mu + viewmat[:, 3].  Depth = Z. */
+typedef struct {
+    float viewmat[12]; /* world -> camera, 3x4 row-major                                      */
+    float fx, fy, cx, cy;
+    float campos[3];   /* camera centre in world space (SH view direction)                   */
+    int32_t width, height;
+    float z_near;      /* keep a Gaussian iff Z >= z_near (0.2 typical)                       */
+    float clip;        /* EWA Jacobian clamp: |X/Z| <= clip * (W/2)/fx (1.3 typical, 0 = off) */
+} ss_camera;
+
+/* One frame's device workspace.  `capacity` = maximum number of (tile, Gaussian) pairs the
+ * workspace holds; `width`/`height` fix the 16x16 tile grid. */
+typedef struct {
+    void *ws;          /* device, ss_frame_workspace_size(n, capacity, width, height) bytes  */
+    size_t ws_bytes;
+    int32_t n;
+    uint32_t capacity;
+    int32_t width, height;
+} ss_frame;
+
+/* Byte offsets of every sub-buffer inside the workspace (for inspection and tests).
+ * Record layout (48 B per Gaussian, AoS float4 x3):
+ *   rec[3i+0] = (x2d, y2d, a, b)   rec[3i+1] = (c, t, sigma, depth)   rec[3i+2] = (r, g, b, 0)
+ * where (a, b, c) is the conic Sigma_2D^-1 (Eq. 10) and t = 2 log(255 sigma) (Eq. 11).
+ * bininfo[i] = (x0 | x1 << 16, y0 | y1 << 16, tile count, 0): the mode's tile rect and count.
+ * Pairs: tile ids are uint16, values are Gaussian indices (uint32). */
+typedef struct {
+    size_t rec;           /* float4 [3n]                                                      */
+    size_t bininfo;       /* uint4  [n]                                                       */
+    size_t depth_key;     /* uint32 [n]   float bits of depth, 0xFFFFFFFF = no tiles          */
+    size_t order;         /* uint32 [n]   visible Gaussians in (depth, index) order           */
+    size_t pair_tile;     /* uint16 [capacity] emitted tile ids (depth order)                 */
+    size_t pair_value;    /* uint32 [capacity] emitted Gaussian ids                           */
+    size_t sorted_value;  /* uint32 [capacity] Gaussian ids sorted by (tile, depth, index)    */
+    size_t tile_count;    /* uint32 [n_tiles]                                                 */
+    size_t ranges;        /* uint32 [n_tiles][2] per tile [start, end) into sorted_value      */
+    size_t n_visible;     /* uint32 [1]   Gaussians with >= 1 tile                            */
+    size_t total_pairs;   /* uint32 [1]   P                                                   */
+    size_t overflow;      /* uint32 [1]   1 iff P > capacity                                  */
+    size_t scratch;       /* internal                                                         */
+    size_t total_bytes;
+    int32_t tiles_x, tiles_y, n_tiles, tile_bits;
+} ss_layout;
+
+SS_API size_t ss_frame_workspace_size(int32_t n, uint32_t capacity, int32_t width, int32_t height);
+SS_API ss_status ss_frame_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height, ss_layout *out /*host*/);
+
+/* a1 -- preprocess (Sec. 3.2.1; count mode of SnugBox/AccuTile).
+ * Per Gaussian: cull (Z < z_near, singular Sigma_2D; in SnugBox/AccuTile also sigma <=
+ * 1/255), project mu, Sigma_3D = R S S^T R^T (Eq. 3), Sigma_2D = J W Sigma_3D W^T J^T + 0.3 I
+ * (Eq. 4), conic, SH colour, t, the mode's tile rect and tile count.  Writes rec, bininfo,
+ * depth_key, n_visible and the depth-digit histograms.  Reads the 16 B mean_opac of every
+ * Gaussian and the rest only for Gaussians in front of the camera. */
+SS_API ss_status ss_preprocess(const ss_scene *scene /*host*/, const ss_camera *cam /*host*/, ss_bin_mode mode,
+                        const ss_frame *frame /*host*/, void *stream);
+
+/* a2+a3 -- key allocation and emission (InclusiveSum + duplicateWithKeys).
+ * Orders the visible Gaussians by (depth bits, index) (stable LSD radix sort, 4 passes),
+ * exclusive-scans their tile counts in that order (decoupled look-back), and emits one
+ * (tile id, Gaussian id) pair per tile of each Gaussian -- the tile set is recomputed from
+ * the stored record by the same function as the count.  Writes order, pair_tile,
+ * pair_value, tile_count, total_pairs, overflow.  Requires ss_preprocess on the frame. */
+SS_API ss_status ss_bin(const ss_camera *cam /*host*/, ss_bin_mode mode, const ss_frame *frame /*host*/, void *stream);
+
+/* a4+a5 -- RadixSort + identifyTileRanges.  Stable LSD radix sort of the
+ * depth-ordered pairs by tile id; the result equals a stable sort of the paper's 64-bit
+ * keys (tile << 32 | depth bits) emitted in Gaussian-index order.  Writes sorted_value and
+ * ranges (empty tiles: [0,0)).  Requires ss_bin on the frame. */
+SS_API ss_status ss_sort(const ss_frame *frame /*host*/, void *stream);
+
+/* Materialise the paper's sorted 64-bit key array (tile << 32 | float bits of depth) from
+ * sorted_value and ranges: keys[P] (device, >= capacity entries).  Inspection only. */
+SS_API ss_status ss_sorted_keys(const ss_frame *frame /*host*/, uint64_t *keys, void *stream);
+
+/* a6 -- render (Sec. 3.2.3, Eqs. 5-7).  One CTA per 16x16 tile; each pixel walks its
+ * tile's depth-ordered list: q = (p-mu)^T Sigma^-1 (p-mu); skip unless q <= t (alpha >=
+ * 1/255, Eq. 9); alpha = min(0.99, sigma e^{-q/2}); stop before blending when T(1-alpha) <
+ * 1e-4; C += c alpha T.  out_rgb = C + T bg, planar float32 [3][H][W].  out_T (float32
+ * [H][W], final transmittance) and out_ncontrib (uint32 [H][W], list entries up to and
+ * including the last blended one) are optional (NULL). bg is host float[3]. */
+SS_API ss_status ss_render(const ss_frame *frame /*host*/, const float *bg /*host [3]*/, float *out_rgb,
+                    float *out_T, uint32_t *out_ncontrib, void *stream);
+
+/* Measurement helper (never on the timed path): work counts of ss_render for the frame,
+ * accumulated into counters (device uint64 [4]): E_pix (per-pixel evaluations until each
+ * pixel terminates), E_blend (evaluations that blend), E_cta (evaluations issued by
+ * CTA-lock-step walking: 256 x Gaussians staged per tile), pixels. */
+SS_API ss_status ss_render_stats(const ss_frame *frame /*host*/, uint64_t *counters, void *stream);
+
+/* a7 -- efficient pruning score (Sec. 4.2.1, Eqs. 20-21):
+ *   score[i] += sum_p sum_ch (sigma_i dC_ch(p)/dalpha_i(p))^2,
+ *   dC/dalpha_i = c_i T_i - (sum_{k>i} c_k alpha_k T_k + bg T_final) / (1 - alpha_i)
+ * over every pixel p where Gaussian i is blended in this frame.  Forward pass per pixel,
+ * then a back-to-front sweep (recursive suffix colour); per-Gaussian partial sums are
+ * reduced in the CTA and added with float64 atomics.  score: float64 [n], accumulated.
+ * Requires ss_sort on the frame. */
+SS_API ss_status ss_prune_score(const ss_frame *frame /*host*/, const float *bg /*host [3]*/, double *score,
+                         void *stream);
+
+/* Convenience: ss_preprocess + ss_bin + ss_sort + ss_render in one call. */
+SS_API ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
+                          const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib, void *stream);
+
+SS_API const char *ss_status_string(ss_status s);
+SS_API const char *ss_last_cuda_error(void);
+SS_API const char *ss_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SS_H */

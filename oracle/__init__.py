@@ -65,6 +65,8 @@ def lib():
             "or_render_unbinned": (None, [vp, vp, u32, i, i, vp, i, i, i, i, vp]),
             "or_prune_score": (None, [vp, vp, vp, i, vp, vp, i, i, i, i]),
             "or_composite_alphas": (None, [i, vp, vp, vp, vp]),
+            "or_render_tiles": (None, [vp, vp, vp, i, i, vp, vp, i, vp, vp, vp]),
+            "or_prune_score_tiles": (None, [vp, vp, vp, i, i, vp, vp, vp, i]),
             "or_frame": (u64, [i, i, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp, vp, vp, u64, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
@@ -264,3 +266,26 @@ def score_views(scene, cams, mode="accutile", bg=(0.0, 0.0, 0.0)) -> np.ndarray:
         f = frame(scene, cam, mode, bg, render=False)
         prune_score(f.rec, f.values, f.ranges, cam.width, cam.height, bg, s)
     return s
+
+
+def render_tiles(rec, values, ranges, width, height, tiles, bg=(0.0, 0.0, 0.0)):
+    """Oracle render of a list of tiles only; pixels outside those tiles are NaN."""
+    img = np.full((3, height, width), np.nan, np.float32)
+    T = np.full((height, width), np.nan, np.float32)
+    nc = np.zeros((height, width), np.uint32)
+    tl = np.ascontiguousarray(tiles, np.int32)
+    lib().or_render_tiles(_p(np.ascontiguousarray(rec, np.float32)), _p(np.ascontiguousarray(values, np.uint32)),
+                          _p(np.ascontiguousarray(ranges, np.uint32)), width, height,
+                          _p(np.asarray(bg, np.float32)), _p(tl), len(tl), _p(img), _p(T), _p(nc))
+    return img, T, nc
+
+
+def prune_score_tiles(rec, values, ranges, width, height, tiles, bg=(0.0, 0.0, 0.0), score=None):
+    rec = np.ascontiguousarray(rec, np.float32)
+    if score is None:
+        score = np.zeros(len(rec), np.float64)
+    tl = np.ascontiguousarray(tiles, np.int32)
+    lib().or_prune_score_tiles(_p(rec), _p(np.ascontiguousarray(values, np.uint32)),
+                               _p(np.ascontiguousarray(ranges, np.uint32)), width, height,
+                               _p(np.asarray(bg, np.float32)), _p(score), _p(tl), len(tl))
+    return score

@@ -721,3 +721,36 @@ uint64_t or_frame(int n, int sh_degree, const float *mean_opac, const float *sca
     if (img) or_render(rec, values, ranges, cam->width, cam->height, bg, img, outT, ncontrib);
     return P;
 }
+
+/* Tiled render / score restricted to a list of tiles (sampled checks at full size; the
+ * per-pixel arithmetic is composite_pixel / the score loop above, unchanged). */
+void or_render_tiles(const float *rec, const uint32_t *values, const uint32_t *ranges, int width, int height,
+                     const float *bg, const int32_t *tiles, int n_list, float *img, float *outT, uint32_t *ncontrib)
+{
+    int tiles_x = (width + TILE - 1) / TILE;
+    for (int k = 0; k < n_list; ++k) {
+        int tile = tiles[k], tx = tile % tiles_x, ty = tile / tiles_x;
+        uint32_t s = ranges[2 * tile], e = ranges[2 * tile + 1];
+        for (int py = ty * TILE; py < ty * TILE + TILE && py < height; ++py)
+            for (int px = tx * TILE; px < tx * TILE + TILE && px < width; ++px) {
+                float rgb[3], T;
+                uint32_t nc = composite_pixel(rec, values + s, e - s, (float)px, (float)py, bg, rgb, &T);
+                size_t p = (size_t)py * width + px;
+                for (int ch = 0; ch < 3; ++ch) img[(size_t)ch * width * height + p] = rgb[ch];
+                if (outT) outT[p] = T;
+                if (ncontrib) ncontrib[p] = nc;
+            }
+    }
+}
+
+void or_prune_score_tiles(const float *rec, const uint32_t *values, const uint32_t *ranges, int width,
+                          int height, const float *bg, double *score, const int32_t *tiles, int n_list)
+{
+    int tiles_x = (width + TILE - 1) / TILE;
+    for (int k = 0; k < n_list; ++k) {
+        int tile = tiles[k], tx = tile % tiles_x, ty = tile / tiles_x;
+        int x1 = tx * TILE + TILE < width ? tx * TILE + TILE : width;
+        int y1 = ty * TILE + TILE < height ? ty * TILE + TILE : height;
+        or_prune_score(rec, values, ranges, width, bg, score, tx * TILE, x1, ty * TILE, y1);
+    }
+}

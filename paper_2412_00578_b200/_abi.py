@@ -1,0 +1,94 @@
+"""ctypes binding of libss.so (include/ss.h).  Argument marshalling only: every step of
+the path runs in libss's CUDA kernels.  There is NO fallback: if libss.so cannot be loaded
+the import raises."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libss.so")
+
+SS_OK, SS_ERR_INVALID_ARG, SS_ERR_CAPACITY, SS_ERR_CUDA, SS_ERR_UNSUPPORTED = range(5)
+MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}
+
+EXPORTS = ["ss_frame_workspace_size", "ss_frame_layout", "ss_preprocess", "ss_bin", "ss_sort", "ss_sorted_keys",
+           "ss_render", "ss_render_stats", "ss_prune_score", "ss_render_frame", "ss_status_string", "ss_last_cuda_error", "ss_version"]
+
+
+class SsScene(C.Structure):
+    _fields_ = [("n", C.c_int32), ("sh_degree", C.c_int32), ("mean_opac", C.c_void_p), ("scale", C.c_void_p),
+                ("rot", C.c_void_p), ("sh", C.c_void_p)]
+
+
+class SsCamera(C.Structure):
+    _fields_ = [("viewmat", C.c_float * 12), ("fx", C.c_float), ("fy", C.c_float), ("cx", C.c_float),
+                ("cy", C.c_float), ("campos", C.c_float * 3), ("width", C.c_int32), ("height", C.c_int32),
+                ("z_near", C.c_float), ("clip", C.c_float)]
+
+
+class SsFrame(C.Structure):
+    _fields_ = [("ws", C.c_void_p), ("ws_bytes", C.c_size_t), ("n", C.c_int32), ("capacity", C.c_uint32),
+                ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class SsLayout(C.Structure):
+    _fields_ = [(k, C.c_size_t) for k in ("rec", "bininfo", "depth_key", "order", "pair_tile", "pair_value",
+                                          "sorted_value", "tile_count", "ranges", "n_visible", "total_pairs",
+                                          "overflow", "scratch", "total_bytes")] + \
+               [(k, C.c_int32) for k in ("tiles_x", "tiles_y", "n_tiles", "tile_bits")]
+
+
+class SsError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SsError(f"libss.so not built ({LIB_PATH}); run `python -m paper_2412_00578_b200.build`")
+        _lib = C.CDLL(LIB_PATH)
+        vp, st = C.c_void_p, C.c_int
+        P = C.POINTER
+        sig = {
+            "ss_frame_workspace_size": (C.c_size_t, [C.c_int32, C.c_uint32, C.c_int32, C.c_int32]),
+            "ss_frame_layout": (st, [C.c_int32, C.c_uint32, C.c_int32, C.c_int32, P(SsLayout)]),
+            "ss_preprocess": (st, [P(SsScene), P(SsCamera), st, P(SsFrame), vp]),
+            "ss_bin": (st, [P(SsCamera), st, P(SsFrame), vp]),
+            "ss_sort": (st, [P(SsFrame), vp]),
+            "ss_sorted_keys": (st, [P(SsFrame), vp, vp]),
+            "ss_render": (st, [P(SsFrame), P(C.c_float), vp, vp, vp, vp]),
+            "ss_render_stats": (st, [P(SsFrame), vp, vp]),
+            "ss_prune_score": (st, [P(SsFrame), P(C.c_float), vp, vp]),
+            "ss_render_frame": (st, [P(SsScene), P(SsCamera), st, P(SsFrame), P(C.c_float), vp, vp, vp, vp]),
+            "ss_status_string": (C.c_char_p, [st]),
+            "ss_last_cuda_error": (C.c_char_p, []),
+            "ss_version": (C.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(_lib, name)
+            fn.restype = res
+            fn.argtypes = args
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != SS_OK:
+        msg = lib().ss_status_string(status).decode()
+        if status == SS_ERR_CUDA:
+            msg += " (" + lib().ss_last_cuda_error().decode() + ")"
+        raise SsError(f"{what}: {msg}")
+
+
+def layout(n: int, capacity: int, width: int, height: int) -> SsLayout:
+    out = SsLayout()
+    check(lib().ss_frame_layout(n, capacity, width, height, C.byref(out)), "ss_frame_layout")
+    return out
+
+
+def workspace_size(n: int, capacity: int, width: int, height: int) -> int:
+    return int(lib().ss_frame_workspace_size(n, capacity, width, height))

@@ -1,0 +1,226 @@
+// ss_api.cu -- the extern "C" boundary of libss.so (declared in include/ss.h).
+// Host-side validation, workspace layout and the launch sequence of each call.
+#include <cstdio>
+#include <cstring>
+
+#include "ss_common.cuh"
+
+namespace ss {
+
+static size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+
+bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height, Layout *L) {
+    if (n < 0 || width <= 0 || height <= 0) return false;
+    std::memset(L, 0, sizeof(*L));
+    ss_layout &P = L->pub;
+    P.tiles_x = (width + kTile - 1) / kTile;
+    P.tiles_y = (height + kTile - 1) / kTile;
+    P.n_tiles = P.tiles_x * P.tiles_y;
+    int bits = 1;
+    while ((1 << bits) < P.n_tiles) ++bits;
+    P.tile_bits = bits;
+    L->tile_passes = bits <= 8 ? 1 : 2;
+    L->n = n;
+    L->capacity = capacity;
+    L->nblk_depth = (uint32_t)(((size_t)n + kSortTile - 1) / kSortTile);
+    L->nblk_tile = (uint32_t)(((size_t)capacity + kSortTile - 1) / kSortTile);
+    L->nblk_emit = (uint32_t)(((size_t)n + kEmitThreads - 1) / kEmitThreads);
+    const size_t N = (size_t)n, Cap = capacity, T = (size_t)P.n_tiles;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        const size_t o = off;
+        off = align_up(off + bytes);
+        return o;
+    };
+    P.rec = take(48 * N);
+    P.bininfo = take(16 * N);
+    P.depth_key = take(4 * N);
+    P.order = take(4 * N);
+    L->dkA = take(4 * N);
+    L->dvA = take(4 * N);
+    L->dkB = take(4 * N);
+    L->dvB = take(4 * N);
+    P.scratch = L->dkA;
+    P.pair_tile = take(2 * Cap);
+    L->pair_tile2 = take(2 * Cap);
+    P.pair_value = take(4 * Cap);
+    L->pair_value2 = take(4 * Cap);
+    P.sorted_value = take(4 * Cap);
+    P.ranges = take(8 * T);
+    // ---- region cleared at the start of every frame
+    L->zero_begin = off;
+    P.tile_count = take(4 * T);
+    P.n_visible = take(4);
+    P.total_pairs = take(4);
+    P.overflow = take(4);
+    L->hist_depth = take(4 * 256 * kDepthPasses);
+    L->hist_tile = take(4 * 256 * 2);
+    L->counters = take(4 * 16);
+    L->lb_depth = take(4 * 256 * (size_t)L->nblk_depth * kDepthPasses);
+    L->lb_tile = take(4 * 256 * (size_t)L->nblk_tile * 2);
+    L->lb_emit = take(4 * (size_t)L->nblk_emit);
+    L->zero_end = off;
+    P.total_bytes = off;
+    return true;
+}
+
+static thread_local char g_cuda_err[256] = "";
+
+static ss_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return SS_OK;
+    std::snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return SS_ERR_CUDA;
+}
+
+static ss_status check_frame(const ss_frame *f, Layout *L) {
+    if (!f || !f->ws) return SS_ERR_INVALID_ARG;
+    if (f->n < 0 || f->width <= 0 || f->height <= 0) return SS_ERR_INVALID_ARG;
+    if (f->n >= (1 << 30) || f->capacity >= (1u << 30)) return SS_ERR_UNSUPPORTED;
+    if (!compute_layout(f->n, f->capacity, f->width, f->height, L)) return SS_ERR_INVALID_ARG;
+    if (L->pub.n_tiles > 65536) return SS_ERR_UNSUPPORTED;
+    if (f->ws_bytes < L->pub.total_bytes) return SS_ERR_INVALID_ARG;
+    return SS_OK;
+}
+
+static ss_status check_cam(const ss_camera *c, const ss_frame *f) {
+    if (!c) return SS_ERR_INVALID_ARG;
+    if (c->width != f->width || c->height != f->height) return SS_ERR_INVALID_ARG;
+    if (!(c->fx > 0.0f) || !(c->fy > 0.0f)) return SS_ERR_INVALID_ARG;
+    return SS_OK;
+}
+
+static CamArgs cam_args(const ss_camera &c, const Layout &L) {
+    CamArgs a;
+    for (int i = 0; i < 12; ++i) a.V[i] = c.viewmat[i];
+    a.fx = c.fx;
+    a.fy = c.fy;
+    a.cx = c.cx;
+    a.cy = c.cy;
+    a.cpx = c.campos[0];
+    a.cpy = c.campos[1];
+    a.cpz = c.campos[2];
+    a.W = c.width;
+    a.H = c.height;
+    a.z_near = c.z_near;
+    a.clip = c.clip;
+    a.tiles_x = L.pub.tiles_x;
+    a.tiles_y = L.pub.tiles_y;
+    return a;
+}
+
+}  // namespace ss
+
+using namespace ss;
+
+extern "C" {
+
+size_t ss_frame_workspace_size(int32_t n, uint32_t capacity, int32_t width, int32_t height) {
+    Layout L;
+    if (!compute_layout(n, capacity, width, height, &L)) return 0;
+    return L.pub.total_bytes;
+}
+
+ss_status ss_frame_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height, ss_layout *out) {
+    if (!out) return SS_ERR_INVALID_ARG;
+    Layout L;
+    if (!compute_layout(n, capacity, width, height, &L)) return SS_ERR_INVALID_ARG;
+    *out = L.pub;
+    return SS_OK;
+}
+
+ss_status ss_preprocess(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
+                        void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    if ((s = check_cam(cam, frame)) != SS_OK) return s;
+    if (!scene || scene->n != frame->n || scene->sh_degree < 0 || scene->sh_degree > 3) return SS_ERR_INVALID_ARG;
+    if (scene->n > 0 && (!scene->mean_opac || !scene->scale || !scene->rot || !scene->sh)) return SS_ERR_INVALID_ARG;
+    if ((int)mode < 0 || (int)mode > 2) return SS_ERR_INVALID_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(at<char>(frame->ws, L.zero_begin), 0, L.zero_end - L.zero_begin, st);
+    if (e != cudaSuccess) return cuda_status(e);
+    return cuda_status(launch_preprocess(*scene, cam_args(*cam, L), (int)mode, frame->ws, L, st));
+}
+
+ss_status ss_bin(const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame, void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    if ((s = check_cam(cam, frame)) != SS_OK) return s;
+    if ((int)mode < 0 || (int)mode > 2) return SS_ERR_INVALID_ARG;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = launch_depth_sort(frame->ws, L, st);
+    if (e == cudaSuccess) e = launch_emit(cam_args(*cam, L), (int)mode, frame->ws, L, st);
+    return cuda_status(e);
+}
+
+ss_status ss_sort(const ss_frame *frame, void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    return cuda_status(launch_tile_sort(frame->ws, L, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_sorted_keys(const ss_frame *frame, uint64_t *keys, void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    if (!keys) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_sorted_keys(frame->ws, L, keys, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_render(const ss_frame *frame, const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib,
+                    void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    if (!bg || !out_rgb) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_render(frame->ws, L, frame->width, frame->height, bg[0], bg[1], bg[2], out_rgb, out_T,
+                                     out_ncontrib, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_render_stats(const ss_frame *frame, uint64_t *counters, void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    if (!counters) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_render_stats(frame->ws, L, frame->width, frame->height,
+                                           reinterpret_cast<unsigned long long *>(counters),
+                                           static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_prune_score(const ss_frame *frame, const float *bg, double *score, void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    if (!bg || (!score && frame->n > 0)) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_prune_score(frame->ws, L, frame->width, frame->height, bg[0], bg[1], bg[2], score,
+                                          static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
+                          const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib, void *stream) {
+    ss_status s = ss_preprocess(scene, cam, mode, frame, stream);
+    if (s == SS_OK) s = ss_bin(cam, mode, frame, stream);
+    if (s == SS_OK) s = ss_sort(frame, stream);
+    if (s == SS_OK) s = ss_render(frame, bg, out_rgb, out_T, out_ncontrib, stream);
+    return s;
+}
+
+const char *ss_status_string(ss_status s) {
+    switch (s) {
+        case SS_OK: return "SS_OK";
+        case SS_ERR_INVALID_ARG: return "SS_ERR_INVALID_ARG";
+        case SS_ERR_CAPACITY: return "SS_ERR_CAPACITY";
+        case SS_ERR_CUDA: return "SS_ERR_CUDA";
+        case SS_ERR_UNSUPPORTED: return "SS_ERR_UNSUPPORTED";
+    }
+    return "SS_UNKNOWN";
+}
+
+const char *ss_last_cuda_error(void) { return g_cuda_err; }
+
+const char *ss_version(void) { return "libss 0.1 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,282 @@
+// ss_sort.cu -- stable LSD radix sort (onesweep, decoupled look-back) and tile ranges.
+//
+// Used twice per frame:
+//   a2  depth order: the visible Gaussians' 32-bit depth keys, 4 x 8-bit passes; pass 0
+//       reads every Gaussian's key (implicit value = index) and drops the 0xFFFFFFFF
+//       sentinel of Gaussians without tiles (compaction fused into the first pass);
+//   a4  tile order: the uint16 tile ids of the depth-ordered pairs, 1-2 x 8-bit passes; the
+//       last pass writes only the Gaussian ids.  Stability makes the result equal to the
+//       paper's stable sort of (tile << 32 | depth) keys.
+// a5 (identifyTileRanges) is the exclusive scan of the per-tile pair counts that
+// the emission kernel histogrammed (k_tile_finalize), so no pass over the keys is needed.
+#include "ss_common.cuh"
+
+namespace ss {
+namespace {
+
+constexpr int kWarps = kSortThreads / 32;
+
+template <typename K>
+__device__ __forceinline__ uint32_t digit_of(K key, int shift) {
+    return (uint32_t)(key >> shift) & 0xFFu;
+}
+
+// One onesweep pass.  Block tickets (atomicAdd) give every CTA tile an id in launch order,
+// so a CTA only waits on ids already owned by running CTAs (forward progress).  Per tile:
+//  1. load 16 keys / thread, warp-striped (warp w owns [w*512, (w+1)*512) of the tile);
+//  2. warp-level stable ranking by 8 ballots per item (match on the digit), per-warp digit
+//     histograms in shared memory;
+//  3. digit totals -> look-back publication (aggregate, then inclusive prefix);
+//  4. scatter into shared memory in tile-sorted order, then write out contiguous digit runs.
+template <typename K, bool IMPLICIT_VALS, bool FILTER, bool WRITE_KEYS>
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__ keys_in,
+                                                           const uint32_t *__restrict__ vals_in,
+                                                           K *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
+                                                           const uint32_t *n_ptr, uint32_t n_fixed, int shift,
+                                                           const uint32_t *__restrict__ digit_count,
+                                                           uint32_t *lookback, uint32_t *ticket) {
+    __shared__ uint32_t s_whist[kWarps][256];
+    __shared__ uint32_t s_digit_base[256];
+    __shared__ uint32_t s_dig_out[256];
+    __shared__ uint32_t s_blk_start[256];
+    __shared__ K s_keys[kSortTile];
+    __shared__ uint32_t s_vals[kSortTile];
+    __shared__ uint32_t s_scan[8];
+    __shared__ uint32_t s_bid;
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t n = n_ptr ? *n_ptr : n_fixed;
+    const uint32_t lanemask_lt = (1u << lane) - 1u;
+    {
+        uint32_t tot;
+        const uint32_t c = digit_count[tid];
+        s_digit_base[tid] = block_exclusive_scan_256(c, s_scan, tot);
+    }
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_bid = atomicAdd(ticket, 1u);
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) s_whist[w][tid] = 0;
+        __syncthreads();
+        const uint32_t bid = s_bid;
+        const size_t base = (size_t)bid * kSortTile;
+        if (base >= n) break;
+
+        K key[kSortItems];
+        uint32_t val[kSortItems];
+        uint32_t rank[kSortItems];
+        uint32_t dig[kSortItems];
+        bool valid[kSortItems];
+        const size_t wbase = base + (size_t)warp * 32 * kSortItems;
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            const size_t idx = wbase + (size_t)j * 32 + lane;
+            valid[j] = idx < n;
+            key[j] = 0;
+            val[j] = 0;
+            if (valid[j]) {
+                key[j] = keys_in[idx];
+                val[j] = IMPLICIT_VALS ? (uint32_t)idx : vals_in[idx];
+                if (FILTER && key[j] == (K)kNoTiles) valid[j] = false;
+            }
+            dig[j] = digit_of(key[j], shift);
+        }
+        // warp-level stable ranking
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            uint32_t peers = __ballot_sync(0xffffffffu, valid[j]);
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const bool bit = (dig[j] >> b) & 1u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bal : ~bal;
+            }
+            const uint32_t lt = __popc(peers & lanemask_lt);
+            uint32_t prev = 0;
+            if (valid[j]) prev = s_whist[warp][dig[j]];
+            __syncwarp();
+            if (valid[j] && lt == 0) s_whist[warp][dig[j]] = prev + __popc(peers);
+            __syncwarp();
+            rank[j] = prev + lt;
+        }
+        __syncthreads();
+        // thread tid owns digit tid: exclusive scan across warps, tile total
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t c = s_whist[w][tid];
+            s_whist[w][tid] = tot;
+            tot += c;
+        }
+        // decoupled look-back for digit tid
+        {
+            volatile uint32_t *lb = lookback + (size_t)bid * 256 + tid;
+            uint32_t prefix = 0;
+            if (bid == 0) {
+                *lb = kFlagInc | tot;
+            } else {
+                *lb = kFlagAgg | tot;
+                const volatile uint32_t *pp = lookback + (size_t)(bid - 1) * 256 + tid;
+                for (;;) {
+                    uint32_t v;
+                    do { v = *pp; } while ((v & ~kValMask) == 0);
+                    prefix += v & kValMask;
+                    if ((v & ~kValMask) == kFlagInc) break;
+                    pp -= 256;
+                }
+                *lb = kFlagInc | (prefix + tot);
+            }
+            s_dig_out[tid] = s_digit_base[tid] + prefix;
+        }
+        uint32_t tile_total;
+        s_blk_start[tid] = block_exclusive_scan_256(tot, s_scan, tile_total);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kSortItems; ++j) {
+            if (valid[j]) {
+                const uint32_t pos = s_blk_start[dig[j]] + s_whist[warp][dig[j]] + rank[j];
+                s_keys[pos] = key[j];
+                s_vals[pos] = val[j];
+            }
+        }
+        __syncthreads();
+        for (uint32_t i = tid; i < tile_total; i += kSortThreads) {
+            const K k = s_keys[i];
+            const uint32_t d = digit_of(k, shift);
+            const uint32_t o = s_dig_out[d] + (i - s_blk_start[d]);
+            if (WRITE_KEYS) keys_out[o] = k;
+            vals_out[o] = s_vals[i];
+        }
+    }
+}
+
+// a5: ranges = exclusive scan of the per-tile pair counts; the digit histograms of the tile
+// passes; the number of pairs to sort (0 on capacity overflow).  One CTA of 1024 threads.
+__global__ void __launch_bounds__(1024) k_tile_finalize(const uint32_t *__restrict__ tile_count, int n_tiles,
+                                                        int passes, const uint32_t *total_pairs,
+                                                        const uint32_t *overflow, uint2 *__restrict__ ranges,
+                                                        uint32_t *__restrict__ hist, uint32_t *sort_n) {
+    __shared__ uint32_t s_hist[2][256];
+    __shared__ uint32_t s_warp[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const bool ovf = *overflow != 0;
+    for (int k = tid; k < 512; k += 1024) (&s_hist[0][0])[k] = 0;
+    __syncthreads();
+    const int per = (n_tiles + 1023) / 1024;
+    const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
+    uint32_t local = 0;
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t c = ovf ? 0u : tile_count[t];
+        local += c;
+        if (c) {
+            atomicAdd(&s_hist[0][t & 0xFF], c);
+            if (passes > 1) atomicAdd(&s_hist[1][(t >> 8) & 0xFF], c);
+        }
+    }
+    uint32_t x = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = s_warp[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        s_warp[lane] = w;
+    }
+    __syncthreads();
+    uint32_t run = (wid ? s_warp[wid - 1] : 0u) + x - local;
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t c = ovf ? 0u : tile_count[t];
+        ranges[t] = c ? make_uint2(run, run + c) : make_uint2(0u, 0u);
+        run += c;
+    }
+    for (int k = tid; k < 512; k += 1024) hist[k] = (&s_hist[0][0])[k];
+    if (tid == 0) *sort_n = ovf ? 0u : *total_pairs;
+}
+
+// The paper's sorted key array, materialised for inspection: keys[j] = tile << 32 | depth.
+__global__ void k_sorted_keys(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ sorted_value,
+                              const float4 *__restrict__ rec, uint64_t *__restrict__ keys) {
+    const int tile = blockIdx.x;
+    const uint2 r = ranges[tile];
+    for (uint32_t j = r.x + threadIdx.x; j < r.y; j += blockDim.x) {
+        const uint32_t g = sorted_value[j];
+        keys[j] = ((uint64_t)tile << 32) | __float_as_uint(rec[3 * (size_t)g + 1].w);
+    }
+}
+
+int sort_grid(uint32_t nblk) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const uint32_t cap = (uint32_t)sms * 4;
+    return (int)(nblk < cap ? (nblk ? nblk : 1) : cap);
+}
+
+}  // namespace
+
+cudaError_t launch_depth_sort(void *ws, const Layout &L, cudaStream_t st) {
+    const ss_layout &P = L.pub;
+    if (L.n == 0) return cudaSuccess;
+    const int grid = sort_grid(L.nblk_depth);
+    uint32_t *hist = at<uint32_t>(ws, L.hist_depth);
+    uint32_t *tick = at<uint32_t>(ws, L.counters);
+    uint32_t *lb = at<uint32_t>(ws, L.lb_depth);
+    const size_t lbs = (size_t)L.nblk_depth * 256;
+    const uint32_t *nvis = at<uint32_t>(ws, P.n_visible);
+    uint32_t *kA = at<uint32_t>(ws, L.dkA), *vA = at<uint32_t>(ws, L.dvA);
+    uint32_t *kB = at<uint32_t>(ws, L.dkB), *vB = at<uint32_t>(ws, L.dvB);
+    k_onesweep<uint32_t, true, true, true><<<grid, kSortThreads, 0, st>>>(
+        at<uint32_t>(ws, P.depth_key), nullptr, kA, vA, nullptr, (uint32_t)L.n, 0, hist, lb, tick + 0);
+    k_onesweep<uint32_t, false, false, true><<<grid, kSortThreads, 0, st>>>(kA, vA, kB, vB, nvis, 0, 8, hist + 256,
+                                                                          lb + lbs, tick + 1);
+    k_onesweep<uint32_t, false, false, true><<<grid, kSortThreads, 0, st>>>(kB, vB, kA, vA, nvis, 0, 16, hist + 512,
+                                                                          lb + 2 * lbs, tick + 2);
+    k_onesweep<uint32_t, false, false, false><<<grid, kSortThreads, 0, st>>>(
+        kA, vA, nullptr, at<uint32_t>(ws, P.order), nvis, 0, 24, hist + 768, lb + 3 * lbs, tick + 3);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_sort(void *ws, const Layout &L, cudaStream_t st) {
+    const ss_layout &P = L.pub;
+    uint32_t *hist = at<uint32_t>(ws, L.hist_tile);
+    uint32_t *tick = at<uint32_t>(ws, L.counters);
+    uint32_t *sort_n = tick + 15;
+    k_tile_finalize<<<1, 1024, 0, st>>>(at<const uint32_t>(ws, P.tile_count), P.n_tiles, L.tile_passes,
+                                        at<const uint32_t>(ws, P.total_pairs), at<const uint32_t>(ws, P.overflow),
+                                        at<uint2>(ws, P.ranges), hist, sort_n);
+    if (L.capacity == 0) return cudaGetLastError();
+    const int grid = sort_grid(L.nblk_tile);
+    uint32_t *lb = at<uint32_t>(ws, L.lb_tile);
+    const size_t lbs = (size_t)L.nblk_tile * 256;
+    uint16_t *k0 = at<uint16_t>(ws, P.pair_tile), *k1 = at<uint16_t>(ws, L.pair_tile2);
+    uint32_t *v0 = at<uint32_t>(ws, P.pair_value), *v1 = at<uint32_t>(ws, L.pair_value2);
+    uint32_t *out = at<uint32_t>(ws, P.sorted_value);
+    if (L.tile_passes == 1) {
+        k_onesweep<uint16_t, false, false, false><<<grid, kSortThreads, 0, st>>>(k0, v0, nullptr, out, sort_n, 0, 0,
+                                                                               hist, lb, tick + 4);
+    } else {
+        k_onesweep<uint16_t, false, false, true><<<grid, kSortThreads, 0, st>>>(k0, v0, k1, v1, sort_n, 0, 0, hist,
+                                                                              lb, tick + 4);
+        k_onesweep<uint16_t, false, false, false><<<grid, kSortThreads, 0, st>>>(k1, v1, nullptr, out, sort_n, 0, 8,
+                                                                               hist + 256, lb + lbs, tick + 5);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sorted_keys(void *ws, const Layout &L, uint64_t *keys, cudaStream_t st) {
+    const ss_layout &P = L.pub;
+    if (P.n_tiles == 0) return cudaSuccess;
+    k_sorted_keys<<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
+                                              at<const float4>(ws, P.rec), keys);
+    return cudaGetLastError();
+}
+
+}  // namespace ss

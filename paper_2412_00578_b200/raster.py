@@ -1,0 +1,200 @@
+"""Public Python API over libss (the five C-ABI calls of include/ss.h).
+
+PyTorch is plumbing only: device memory (the scene planes, the frame workspace, outputs)
+and the current CUDA stream.  Every computation runs in libss's kernels; there is no CPU
+or PyTorch fallback -- constructing a Rasterizer without a CUDA device or without
+libss.so raises.
+
+    scene = DeviceScene.from_host(synth_scene)            # SoA planes -> HBM
+    rz = Rasterizer(scene, width, height, mode="accutile")
+    img = rz.render_frame(camera)                         # [3, H, W] float32 on the device
+    rz.prune_score(score)                                 # score[i] += U~_i for that frame
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._abi import MODES, SsCamera, SsFrame, SsScene, check, lib
+
+
+@dataclass
+class DeviceScene:
+    mean_opac: torch.Tensor   # [N,4] f32 cuda
+    scale: torch.Tensor       # [N,4]
+    rot: torch.Tensor         # [N,4]
+    sh: torch.Tensor          # [P,N,4]
+    sh_degree: int
+
+    @property
+    def n(self) -> int:
+        return int(self.mean_opac.shape[0])
+
+    @staticmethod
+    def from_host(scene, device="cuda") -> "DeviceScene":
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
+        return DeviceScene(t(scene.mean_opac), t(scene.scale), t(scene.rot), t(scene.sh), int(scene.sh_degree))
+
+    def struct(self) -> SsScene:
+        return SsScene(self.n, self.sh_degree, self.mean_opac.data_ptr(), self.scale.data_ptr(),
+                       self.rot.data_ptr(), self.sh.data_ptr())
+
+
+def camera_struct(cam) -> SsCamera:
+    c = SsCamera()
+    c.viewmat[:] = [float(v) for v in np.asarray(cam.viewmat, np.float32).reshape(-1)]
+    c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
+    c.campos[:] = [float(v) for v in np.asarray(cam.campos, np.float32)]
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.z_near, c.clip = float(cam.z_near), float(cam.clip)
+    return c
+
+
+def _stream_handle(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+class Rasterizer:
+    """One frame workspace (HBM) for a scene and an image size; reusable across views."""
+
+    def __init__(self, scene: DeviceScene, width: int, height: int, mode: str = "accutile",
+                 capacity: int | None = None, device=None):
+        if not torch.cuda.is_available():
+            raise _abi.SsError("libss requires a CUDA device (no CPU fallback)")
+        lib()  # fail loudly if libss.so is missing
+        self.scene = scene
+        self.width, self.height = int(width), int(height)
+        self.mode = mode
+        self.device = device or scene.mean_opac.device
+        self._scene_struct = scene.struct()
+        self.capacity = 0
+        self._alloc(capacity if capacity is not None else max(1024, 4 * scene.n))
+
+    # ---------------------------------------------------------------- workspace
+    def _alloc(self, capacity: int) -> None:
+        capacity = int(min(capacity, (1 << 30) - 1))
+        nbytes = _abi.workspace_size(self.scene.n, capacity, self.width, self.height)
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        self.capacity = capacity
+        self.layout = _abi.layout(self.scene.n, capacity, self.width, self.height)
+        self.frame = SsFrame(self.ws.data_ptr(), nbytes, self.scene.n, capacity, self.width, self.height)
+        self.n_tiles = self.layout.n_tiles
+
+    def _view(self, off: int, count: int, dtype: torch.dtype) -> torch.Tensor:
+        itemsize = torch.tensor([], dtype=dtype).element_size()
+        return self.ws[off: off + count * itemsize].view(dtype)
+
+    # views of the intermediates (zero-copy)
+    def records(self) -> torch.Tensor:
+        return self._view(self.layout.rec, 12 * self.scene.n, torch.float32).view(self.scene.n, 12)
+
+    def bininfo(self) -> torch.Tensor:
+        return self._view(self.layout.bininfo, 4 * self.scene.n, torch.int32).view(self.scene.n, 4)
+
+    def counts(self) -> torch.Tensor:
+        return self.bininfo()[:, 2]
+
+    def order(self) -> torch.Tensor:
+        return self._view(self.layout.order, self.scene.n, torch.int32)
+
+    def pair_tiles(self) -> torch.Tensor:
+        return self._view(self.layout.pair_tile, self.capacity, torch.int16)
+
+    def pair_values(self) -> torch.Tensor:
+        return self._view(self.layout.pair_value, self.capacity, torch.int32)
+
+    def sorted_values(self) -> torch.Tensor:
+        return self._view(self.layout.sorted_value, self.capacity, torch.int32)
+
+    def ranges(self) -> torch.Tensor:
+        return self._view(self.layout.ranges, 2 * self.n_tiles, torch.int32).view(self.n_tiles, 2)
+
+    def tile_counts(self) -> torch.Tensor:
+        return self._view(self.layout.tile_count, self.n_tiles, torch.int32)
+
+    def totals(self) -> dict:
+        """Device counters (synchronises): visible Gaussians, pairs P, overflow flag."""
+        nv = int(self._view(self.layout.n_visible, 1, torch.int32).item())
+        P = int(self._view(self.layout.total_pairs, 1, torch.int32).item()) & 0xFFFFFFFF
+        ov = int(self._view(self.layout.overflow, 1, torch.int32).item())
+        return {"n_visible": nv, "pairs": P, "overflow": ov}
+
+    # ---------------------------------------------------------------- the five calls
+    def preprocess(self, cam, stream=None) -> None:
+        self._cam = camera_struct(cam)
+        check(lib().ss_preprocess(C.byref(self._scene_struct), C.byref(self._cam), MODES[self.mode],
+                                  C.byref(self.frame), C.c_void_p(_stream_handle(stream))), "ss_preprocess")
+
+    def bin(self, cam=None, stream=None) -> None:
+        c = camera_struct(cam) if cam is not None else self._cam
+        check(lib().ss_bin(C.byref(c), MODES[self.mode], C.byref(self.frame),
+                           C.c_void_p(_stream_handle(stream))), "ss_bin")
+
+    def sort(self, stream=None) -> None:
+        check(lib().ss_sort(C.byref(self.frame), C.c_void_p(_stream_handle(stream))), "ss_sort")
+
+    def sorted_keys(self, stream=None) -> torch.Tensor:
+        keys = torch.zeros(max(1, self.capacity), dtype=torch.int64, device=self.device)
+        check(lib().ss_sorted_keys(C.byref(self.frame), C.c_void_p(keys.data_ptr()),
+                                   C.c_void_p(_stream_handle(stream))), "ss_sorted_keys")
+        return keys
+
+    def render(self, bg=(0.0, 0.0, 0.0), out: torch.Tensor | None = None, want_T=False, want_ncontrib=False,
+               stream=None):
+        if out is None:
+            out = torch.empty((3, self.height, self.width), dtype=torch.float32, device=self.device)
+        T = torch.empty((self.height, self.width), dtype=torch.float32, device=self.device) if want_T else None
+        nc = torch.empty((self.height, self.width), dtype=torch.int32, device=self.device) if want_ncontrib else None
+        bgv = (C.c_float * 3)(*[float(v) for v in bg])
+        check(lib().ss_render(C.byref(self.frame), bgv, C.c_void_p(out.data_ptr()),
+                              C.c_void_p(T.data_ptr() if T is not None else 0),
+                              C.c_void_p(nc.data_ptr() if nc is not None else 0),
+                              C.c_void_p(_stream_handle(stream))), "ss_render")
+        if want_T or want_ncontrib:
+            return out, T, nc
+        return out
+
+    def render_stats(self, stream=None) -> dict:
+        """Work counts of the render for the current frame (measurement; synchronises)."""
+        c = torch.zeros(4, dtype=torch.int64, device=self.device)
+        check(lib().ss_render_stats(C.byref(self.frame), C.c_void_p(c.data_ptr()),
+                                    C.c_void_p(_stream_handle(stream))), "ss_render_stats")
+        v = c.cpu().tolist()
+        return {"E_pix": v[0], "E_blend": v[1], "E_cta": v[2], "pixels": v[3]}
+
+    def prune_score(self, score: torch.Tensor, bg=(0.0, 0.0, 0.0), stream=None) -> torch.Tensor:
+        assert score.dtype == torch.float64 and score.numel() == self.scene.n and score.is_cuda
+        bgv = (C.c_float * 3)(*[float(v) for v in bg])
+        check(lib().ss_prune_score(C.byref(self.frame), bgv, C.c_void_p(score.data_ptr()),
+                                   C.c_void_p(_stream_handle(stream))), "ss_prune_score")
+        return score
+
+    # ---------------------------------------------------------------- conveniences
+    def prepare(self, cam, stream=None) -> None:
+        """a1-a5 for one view (preprocess, bin, sort)."""
+        self.preprocess(cam, stream)
+        self.bin(cam, stream)
+        self.sort(stream)
+
+    def ensure_capacity(self, cam, headroom: float = 1.25) -> int:
+        """Run a1-a3 once, read P back (synchronises) and grow the pair capacity if needed."""
+        self.preprocess(cam)
+        self.bin(cam)
+        P = self.totals()["pairs"]
+        if P > self.capacity:
+            self._alloc(int(P * headroom) + 1024)
+        return P
+
+    def render_frame(self, cam, bg=(0.0, 0.0, 0.0), out=None, check_overflow=True, stream=None, **kw):
+        """Full forward frame.  With check_overflow the pair count is read back and the
+        frame re-run once with a larger workspace if the capacity was exceeded."""
+        self.prepare(cam, stream)
+        if check_overflow and self.totals()["overflow"]:
+            self._alloc(int(self.totals()["pairs"] * 1.25) + 1024)
+            self.prepare(cam, stream)
+        return self.render(bg, out, stream=stream, **kw)
