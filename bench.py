@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the Speedy-Splat forward hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload mnr360-3m] [--mode accutile] [--views-per-step V]
+
+A STEP is one batch of V camera views per rank, each rendered through the whole forward
+path a1-a6 (ss_preprocess -> ss_bin -> ss_sort -> ss_render) with the scene resident in
+HBM; `value` = frames rendered by all ranks / max-over-ranks device time.  The scene
+(720 MB for mnr360-3m) and each frame's records (~100 MB) are larger than the 126 MB L2,
+so no explicit L2 flush is needed between steps.  The pruning-score pass (a7 + the NCCL
+all_reduce) is timed in the same run and reported in "prune_score".  Under torchrun every
+rank renders its round-robin shard of the views (weak scaling: V views per rank per step).
+
+--impl reference runs the CPU oracle (oracle/, plain C, the slow checker) on the host's
+cores on the same workload: each step renders one full view per worker process.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP32_LANES_PER_SM = 128  # B200: 4 SMSPs x 32 FP32 lanes (FFMA = 2 flop)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="mnr360-3m")
+    ap.add_argument("--mode", default="accutile", choices=["3sigma", "snugbox", "accutile"])
+    ap.add_argument("--views-per-step", type=int, default=64)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-score", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="short run for profilers: no clocks/e2e/cpu legs")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampled DURING the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        rows = [r.split(", ") for r in out.strip().splitlines() if r.count(",") >= 8]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[5 + k].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------ oracle (CPU)
+_POOL_SCENE = None
+
+
+def _oracle_frame_worker(args):
+    import oracle
+    name, view, mode = args
+    cams = _POOL_SCENE[1]
+    t0 = time.perf_counter()
+    f = oracle.frame(_POOL_SCENE[0], cams[view], mode, cap_hint=6 * _POOL_SCENE[0].n)
+    return time.perf_counter() - t0, f.P
+
+
+def oracle_pool(name, mode, workers):
+    """Fork a pool of `workers` processes sharing the generated scene (copy-on-write)."""
+    global _POOL_SCENE
+    import multiprocessing as mp
+
+    from paper_2412_00578_b200 import synth
+    if _POOL_SCENE is None:
+        _POOL_SCENE = synth.make_workload(name)
+    import oracle
+    oracle.build()
+    ctx = mp.get_context("fork")
+    return ctx.Pool(workers)
+
+
+def run_oracle_steps(name, mode, steps, warmup, workers):
+    """Each step: `workers` full oracle frames in parallel (one view per worker process)."""
+    pool = oracle_pool(name, mode, workers)
+    n_views = len(_POOL_SCENE[1])
+    v = 0
+    times = []
+    pairs = []
+    for k in range(warmup + steps):
+        jobs = [(name, (v + j) % n_views, mode) for j in range(workers)]
+        v += workers
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_frame_worker, jobs)
+        dt = time.perf_counter() - t0
+        if k >= warmup:
+            times.append(dt)
+            pairs += [r[1] for r in res]
+    pool.close()
+    pool.join()
+    total = sum(times)
+    return {"value": steps * workers / total, "ms_per_step": 1e3 * total / steps, "pairs": pairs,
+            "frames": steps * workers}
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return 0
+    workers = max(1, min(8, host_cores()))
+    r = run_oracle_steps(args.workload, args.mode, args.steps, args.warmup, workers)
+    line = {
+        "impl": "reference", "metric": "rendered frames/sec (forward a1-a6)", "value": r["value"],
+        "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic", "config": {"workload": args.workload, "mode": args.mode},
+        "pairs_per_frame": statistics.mean(r["pairs"]) if r["pairs"] else None,
+        "cpu_baseline": {"value": r["value"], "unit": "frames/s", "cores": workers, "kind": "oracle",
+                         "sample": f"{r['frames']} full views of {args.workload} ({workers} worker processes, "
+                                   f"one view each per step; oracle/ss_oracle.c -O2 -ffp-contract=off)"},
+        "e2e": {"value": r["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ ours (GPU)
+def stage_bytes(stage, N, n_vis, P, n_tiles, W, H, sh_floats):
+    """Algorithmic bytes per launch: what the step must move at minimum."""
+    if stage == "preprocess":
+        return 16 * N + (32 + 4 * sh_floats) * n_vis + 48 * n_vis + 4 * N
+    if stage == "bin":       # emit: read the needed record fields + count, write (tile u16, id u32)
+        return 4 * N + (28 + 4) * n_vis + 6 * P
+    if stage == "sort":      # read each pair once, write the sorted id once, ranges
+        return 6 * P + 4 * P + 8 * n_tiles
+    if stage == "render":    # id + gathered record (36 B used) per pair, image
+        return 40 * P + 12 * W * H
+    raise KeyError(stage)
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_2412_00578_b200 import dist, synth
+    from paper_2412_00578_b200._abi import SsCamera
+    from paper_2412_00578_b200.raster import DeviceScene, Rasterizer, render_views_to_host
+
+    rank, world, local = dist.init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    scene, cams = synth.make_workload(args.workload)
+    W, H = cams[0].width, cams[0].height
+    my_views = dist.views_for_rank(len(cams), rank, world)
+    if args.ncu:
+        my_views = my_views[:4]
+    ds = DeviceScene.from_host(scene, dev)
+    rz = Rasterizer(ds, W, H, mode=args.mode, capacity=max(1024, 4 * scene.n))
+
+    # sizing + per-view statistics (untimed): pairs per frame, visible counts, render work
+    pairs, nvis, E_pix, E_blend, E_cta = {}, {}, {}, {}, {}
+    for v in my_views:
+        rz.ensure_capacity(cams[v])
+    cap = rz.capacity
+    for v in my_views:
+        rz.prepare(cams[v])
+        rz.render()
+        t = rz.totals()
+        assert not t["overflow"]
+        pairs[v], nvis[v] = t["pairs"], t["n_visible"]
+        st = rz.render_stats()
+        E_pix[v], E_blend[v], E_cta[v] = st["E_pix"], st["E_blend"], st["E_cta"]
+    # shrink capacity to the measured maximum (+2%) so the per-frame memset is tight
+    rz._alloc(int(max(pairs.values()) * 1.02) + 4096)
+
+    V = args.views_per_step
+    seq = [my_views[j % len(my_views)] for j in range((args.warmup + args.steps) * V)]
+    out = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    stages = ["preprocess", "bin", "sort", "render"]
+    n_timed = args.steps * V
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(n_timed)]
+
+    def frame(v, e=None):
+        cam = cams[v]
+        if e is not None:
+            e[0].record(stream)
+        rz.preprocess(cam)
+        if e is not None:
+            e[1].record(stream)
+        rz.bin(cam)
+        if e is not None:
+            e[2].record(stream)
+        rz.sort()
+        if e is not None:
+            e[3].record(stream)
+        rz.render(out=out)
+        if e is not None:
+            e[4].record(stream)
+
+    for j in range(args.warmup * V):
+        frame(seq[j])
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    if not args.ncu:
+        clocks.start()
+        time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    timed_views = seq[args.warmup * V:]
+    for j, v in enumerate(timed_views):
+        frame(v, ev[j])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop() if not args.ncu else {}
+    ms_total = t_start.elapsed_time(t_end)
+    ms_max = dist.max_over_ranks(ms_total)
+    value = world * n_timed / (ms_max / 1e3)
+    stage_ms = {s: sum(ev[j][i].elapsed_time(ev[j][i + 1]) for j in range(n_timed)) / n_timed
+                for i, s in enumerate(stages)}
+
+    # ---- per-stage roofline numbers (averages over the timed frames)
+    mean = lambda d: float(np.mean([d[v] for v in timed_views]))
+    Pm, NVm = mean(pairs), mean(nvis)
+    sh_floats = {0: 4, 1: 12, 2: 28, 3: 48}[scene.sh_degree]
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * FP32_LANES_PER_SM * 2 * sm_max * 1e6 / 1e12
+    stage_info = {}
+    for s in stages:
+        if s == "render":
+            flops = 9.0 * mean(E_pix) + 10.0 * mean(E_blend)
+            ach = flops / (stage_ms[s] / 1e3) / 1e12
+            stage_info[s] = {"ms": stage_ms[s], "bound": "alu", "achieved": ach, "peak": fp32_peak,
+                             "unit": "TFLOP/s", "frac": ach / fp32_peak,
+                             "gbs_algorithmic": stage_bytes(s, scene.n, NVm, Pm, rz.n_tiles, W, H, sh_floats)
+                             / (stage_ms[s] / 1e3) / 1e9}
+        else:
+            b = stage_bytes(s, scene.n, NVm, Pm, rz.n_tiles, W, H, sh_floats)
+            ach = b / (stage_ms[s] / 1e3) / 1e9
+            stage_info[s] = {"ms": stage_ms[s], "bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                             "unit": "GB/s", "frac": ach / hbm_peak, "bytes": b}
+    dom = max(stages, key=lambda s: stage_ms[s])
+    di = stage_info[dom]
+    roof = {"bound": di["bound"], "achieved": di["achieved"], "peak": di["peak"], "unit": di["unit"],
+            "frac": di["frac"], "traffic": None, "kernel": dom,
+            "peak_source": hbm_src if di["bound"] == "hbm" else
+            f"derived: 148 SM x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {sm_max:.0f} MHz"}
+
+    # ---- pruning-score pass (a1-a5 + a7 over this rank's views, then the NCCL all_reduce)
+    score_info = None
+    if not args.no_score and not args.ncu:
+        score = torch.zeros(scene.n, dtype=torch.float64, device=dev)
+        n_sv = min(len(my_views), 2 * V)
+        for v in my_views[:4]:
+            rz.prepare(cams[v])
+            rz.prune_score(score)
+        score.zero_()
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(stream)
+        for v in my_views[:n_sv]:
+            rz.prepare(cams[v])
+            rz.prune_score(score)
+        b.record(stream)
+        dist.allreduce_scores(score)
+        c.record(stream)
+        torch.cuda.synchronize()
+        ms_s = dist.max_over_ranks(a.elapsed_time(c))
+        score_info = {"views_per_s": world * n_sv / (ms_s / 1e3), "views": world * n_sv,
+                      "ms_score_views": a.elapsed_time(b), "ms_allreduce": b.elapsed_time(c),
+                      "allreduce_bytes": 8 * scene.n, "dtype": "f64 accumulate, f32 per-pixel"}
+
+    # ---- end to end through the public API: camera in, image out to pinned host memory
+    e2e = None
+    if not args.no_e2e and not args.ncu:
+        n_e = min(len(my_views), V)
+        host = [torch.empty((3, H, W), dtype=torch.float32).pin_memory() for _ in range(n_e)]
+        vs = [cams[v] for v in my_views[:n_e]]
+        render_views_to_host(rz, vs, host)
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        reps = max(1, args.steps // 4)
+        for _ in range(reps):
+            render_views_to_host(rz, vs, host)
+        dt = dist.max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": world * reps * n_e / dt, "unit": "frames/s",
+               "h2d_bytes_per_step": V * ctypes.sizeof(SsCamera), "d2h_bytes_per_step": V * 3 * H * W * 4,
+               "note": "scene resident in HBM; per frame the camera goes host->device as kernel arguments and "
+                       "the float32 image device->host into pinned memory (copy overlapped on a side stream)"}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.ncu:
+        workers = max(1, min(8, host_cores()))
+        r = run_oracle_steps(args.workload, args.mode, 1, 0, workers)
+        cpu = {"value": r["value"], "unit": "frames/s", "cores": workers, "kind": "oracle",
+               "sample": f"{r['frames']} full views of {args.workload} (project, bin, sort, render; one view per "
+                         f"worker process)"}
+
+    if rank == 0:
+        line = {
+            "metric": "rendered frames/sec (forward a1-a6) & Gaussian-tile pairs/frame, "
+                      "3M-Gaussian MipNeRF360-shaped",
+            "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": args.workload, "n_gaussians": scene.n, "width": W, "height": H,
+                       "views": len(cams), "views_per_step_per_rank": V, "mode": args.mode,
+                       "sh_degree": scene.sh_degree, "parallelism": f"view-parallel x{world}",
+                       "l2": "no flush: scene (%.0f MB) and per-frame records (%.0f MB) exceed the 126 MB L2"
+                             % (scene.n * 240 / 1e6, NVm * 48 / 1e6)},
+            "pairs_per_frame": {"mean": Pm, "min": min(pairs.values()), "max": max(pairs.values())},
+            "pairs_per_s": value * Pm,
+            "visible_per_frame": NVm,
+            "stages_ms": {s: stage_ms[s] for s in stages},
+            "stages": stage_info,
+            "render_work": {"E_pix": mean(E_pix), "E_blend": mean(E_blend), "E_cta": mean(E_cta),
+                            "pixels": W * H},
+            "roofline": roof,
+            # ours per frame: preprocess 1, bin 4 depth passes + emit, finalize 1, tile passes, render 1
+            "gpu_launches": n_timed * (1 + 5 + 1 + (1 if rz.layout.tile_bits <= 8 else 2) + 1),
+            "clocks": clk,
+            "e2e": e2e,
+            "prune_score": score_info,
+            "cpu_baseline": cpu,
+            "paper_context": {"gpu": "RTX A5000 (PAPER.md P:447)", "accutile_fps_avg_scene": 267,
+                              "speedups": {"snugbox": 1.82, "accutile": 1.99, "overall": 6.71}},
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

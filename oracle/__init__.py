@@ -187,7 +187,7 @@ class Frame:
         self.__dict__.update(kw)
 
 
-def frame(scene, cam, mode: str = "accutile", bg=(0.0, 0.0, 0.0), render=True) -> Frame:
+def frame(scene, cam, mode: str = "accutile", bg=(0.0, 0.0, 0.0), render=True, cap_hint=None) -> Frame:
     n = scene.n
     rec = np.zeros((n, R_NF), np.float32)
     rect = np.zeros((n, 4), np.int32)
@@ -197,9 +197,9 @@ def frame(scene, cam, mode: str = "accutile", bg=(0.0, 0.0, 0.0), render=True) -
     ranges = np.zeros((n_tiles, 2), np.uint32)
     bgv = np.asarray(bg, np.float32)
     oc = camera(cam)
-    cap = 0
-    keys = np.zeros(1, np.uint64)
-    vals = np.zeros(1, np.uint32)
+    cap = int(cap_hint) if cap_hint else 0
+    keys = np.zeros(max(cap, 1), np.uint64)
+    vals = np.zeros(max(cap, 1), np.uint32)
     img = np.zeros((3, cam.height, cam.width), np.float32) if render else None
     T = np.zeros((cam.height, cam.width), np.float32) if render else None
     nc = np.zeros((cam.height, cam.width), np.uint32) if render else None

@@ -198,3 +198,29 @@ class Rasterizer:
             self._alloc(int(self.totals()["pairs"] * 1.25) + 1024)
             self.prepare(cam, stream)
         return self.render(bg, out, stream=stream, **kw)
+
+
+def render_views_to_host(rz: Rasterizer, cams, host_out: list, bg=(0.0, 0.0, 0.0)) -> None:
+    """End-to-end public call: render each camera and land its image in pinned host memory.
+
+    Frame j renders on the current stream into one of two device buffers; its device->host
+    copy runs on a side stream, overlapping frame j+1's kernels.  Returns after the last
+    copy completes.  host_out[j] must be pinned float32 [3, H, W] tensors."""
+    cur = torch.cuda.current_stream()
+    if not hasattr(rz, "_e2e"):
+        rz._e2e = dict(copy=torch.cuda.Stream(device=rz.device),
+                       dev=[torch.empty((3, rz.height, rz.width), dtype=torch.float32, device=rz.device)
+                            for _ in range(2)],
+                       done=[torch.cuda.Event(), torch.cuda.Event()], ready=[torch.cuda.Event(), torch.cuda.Event()])
+    st = rz._e2e
+    for j, cam in enumerate(cams):
+        b = j & 1
+        cur.wait_event(st["done"][b])            # device buffer b free again
+        rz.prepare(cam)
+        rz.render(bg, out=st["dev"][b])
+        st["ready"][b].record(cur)
+        with torch.cuda.stream(st["copy"]):
+            st["copy"].wait_event(st["ready"][b])
+            host_out[j].copy_(st["dev"][b], non_blocking=True)
+            st["done"][b].record(st["copy"])
+    st["copy"].synchronize()
