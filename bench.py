@@ -194,7 +194,7 @@ def run_ours(args):
     rz = Rasterizer(ds, W, H, mode=args.mode, capacity=max(1024, 4 * scene.n))
 
     # sizing + per-view statistics (untimed): pairs per frame, visible counts, render work
-    pairs, nvis, E_pix, E_blend, E_cta = {}, {}, {}, {}, {}
+    pairs, nvis, E_pix, E_blend, E_cta, E_kept = {}, {}, {}, {}, {}, {}
     for v in my_views:
         rz.ensure_capacity(cams[v])
     cap = rz.capacity
@@ -205,7 +205,7 @@ def run_ours(args):
         assert not t["overflow"]
         pairs[v], nvis[v] = t["pairs"], t["n_visible"]
         st = rz.render_stats()
-        E_pix[v], E_blend[v], E_cta[v] = st["E_pix"], st["E_blend"], st["E_cta"]
+        E_pix[v], E_blend[v], E_cta[v], E_kept[v] = st["E_pix"], st["E_blend"], st["E_cta"], st["E_kept"]
     # shrink capacity to the measured maximum (+2%) so the per-frame memset is tight
     rz._alloc(int(max(pairs.values()) * 1.02) + 4096)
 
@@ -361,7 +361,7 @@ def run_ours(args):
             "stages_ms": {s: stage_ms[s] for s in stages},
             "stages": stage_info,
             "render_work": {"E_pix": mean(E_pix), "E_blend": mean(E_blend), "E_cta": mean(E_cta),
-                            "pixels": W * H},
+                            "E_kept_after_warp_cull": mean(E_kept), "pixels": W * H},
             "roofline": roof,
             # ours per frame: preprocess 1, bin 4 depth passes + emit, finalize 1, tile passes, render 1
             "gpu_launches": n_timed * (1 + 5 + 1 + (1 if rz.layout.tile_bits <= 8 else 2) + 1),

@@ -27,7 +27,7 @@
  *   - Errors: host-side validation happens before any launch and returns
  *     SS_ERR_INVALID_ARG (null required pointer, n < 0, width/height <= 0, sh_degree not in
  *     0..3, workspace too small, mode out of range) or SS_ERR_UNSUPPORTED (more than 65536
- *     tiles, n or capacity >= 2^30).  A failed launch returns SS_ERR_CUDA (the CUDA error
+ *     tiles or more than 256 tiles along an axis, n or capacity >= 2^30).  A failed launch returns SS_ERR_CUDA (the CUDA error
  *     string is available from ss_last_cuda_error of the same thread).  Device-side faults
  *     surface on the caller's next synchronisation.  Pair-array overflow is NOT an error
  *     code: ss_bin writes min(P, capacity) pairs, stores P in the workspace's total_pairs
@@ -100,14 +100,19 @@ typedef struct {
 } ss_frame;
 
 /* Byte offsets of every sub-buffer inside the workspace (for inspection and tests).
- * Record layout (48 B per Gaussian, AoS float4 x3):
- *   rec[3i+0] = (x2d, y2d, a, b)   rec[3i+1] = (c, t, sigma, depth)   rec[3i+2] = (r, g, b, 0)
- * where (a, b, c) is the conic Sigma_2D^-1 (Eq. 10) and t = 2 log(255 sigma) (Eq. 11).
- * bininfo[i] = (x0 | x1 << 16, y0 | y1 << 16, tile count, 0): the mode's tile rect and count.
- * Pairs: tile ids are uint16, values are Gaussian indices (uint32). */
+ * Records of a Gaussian with >= 1 tile (written only for those):
+ *   rec  (48 B, render): q0 = (x2d, y2d, a, b), q1 = (c, t, sigma, hx), q2 = (hy, r, g, b)
+ *        (a, b, c) = conic Sigma_2D^-1 (Eq. 10); t = 2 log(255 sigma) (Eq. 11); (hx, hy) =
+ *        SnugBox half-extents widened by the float32 error bound of the render's q
+ *   erec (32 B, emission, one aligned sector): e0 = (count, info, span0, span1),
+ *        e1 = (span2, span3, aux0, aux1); info = nspans | inline << 8 | columns << 9; a span
+ *        is first tile (16 b) | length << 16 | column-step << 31; aux = t as float64 bits
+ *        (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1) (3-sigma / SnugBox).
+ * Depth lives in depth_key (float bits, 0xFFFFFFFF = no tiles).  Pairs: tile ids are
+ * uint16, values are Gaussian indices (uint32). */
 typedef struct {
-    size_t rec;           /* float4 [3n]                                                      */
-    size_t bininfo;       /* uint4  [n]                                                       */
+    size_t rec;           /* float4 [3n]  render records                                      */
+    size_t erec;          /* uint4  [2n]  emission records                                    */
     size_t depth_key;     /* uint32 [n]   float bits of depth, 0xFFFFFFFF = no tiles          */
     size_t order;         /* uint32 [n]   visible Gaussians in (depth, index) order           */
     size_t pair_tile;     /* uint16 [capacity] emitted tile ids (depth order)                 */
@@ -129,7 +134,7 @@ SS_API ss_status ss_frame_layout(int32_t n, uint32_t capacity, int32_t width, in
 /* a1 -- preprocess (Sec. 3.2.1; count mode of SnugBox/AccuTile).
  * Per Gaussian: cull (Z < z_near, singular Sigma_2D; in SnugBox/AccuTile also sigma <=
  * 1/255), project mu, Sigma_3D = R S S^T R^T (Eq. 3), Sigma_2D = J W Sigma_3D W^T J^T + 0.3 I
- * (Eq. 4), conic, SH colour, t, the mode's tile rect and tile count.  Writes rec, bininfo,
+ * (Eq. 4), conic, SH colour, t, the mode's tile rect and tile count.  Writes rec,
  * depth_key, n_visible and the depth-digit histograms.  Reads the 16 B mean_opac of every
  * Gaussian and the rest only for Gaussians in front of the camera. */
 SS_API ss_status ss_preprocess(const ss_scene *scene /*host*/, const ss_camera *cam /*host*/, ss_bin_mode mode,
@@ -163,9 +168,10 @@ SS_API ss_status ss_render(const ss_frame *frame /*host*/, const float *bg /*hos
                     float *out_T, uint32_t *out_ncontrib, void *stream);
 
 /* Measurement helper (never on the timed path): work counts of ss_render for the frame,
- * accumulated into counters (device uint64 [4]): E_pix (per-pixel evaluations until each
- * pixel terminates), E_blend (evaluations that blend), E_cta (evaluations issued by
- * CTA-lock-step walking: 256 x Gaussians staged per tile), pixels. */
+ * accumulated into counters (device uint64 [5]): E_pix (per-pixel evaluations until each
+ * pixel terminates: the method's work), E_blend (evaluations that blend), E_cta (evaluations
+ * issued by CTA-lock-step walking: 256 x Gaussians staged per tile), pixels, E_kept
+ * (evaluations left after the lossless per-warp culling). */
 SS_API ss_status ss_render_stats(const ss_frame *frame /*host*/, uint64_t *counters, void *stream);
 
 /* a7 -- efficient pruning score (Sec. 4.2.1, Eqs. 20-21):

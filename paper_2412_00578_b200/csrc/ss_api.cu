@@ -33,7 +33,7 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
         return o;
     };
     P.rec = take(48 * N);
-    P.bininfo = take(16 * N);
+    P.erec = take(32 * N);
     P.depth_key = take(4 * N);
     P.order = take(4 * N);
     L->dkA = take(4 * N);
@@ -77,7 +77,7 @@ static ss_status check_frame(const ss_frame *f, Layout *L) {
     if (f->n < 0 || f->width <= 0 || f->height <= 0) return SS_ERR_INVALID_ARG;
     if (f->n >= (1 << 30) || f->capacity >= (1u << 30)) return SS_ERR_UNSUPPORTED;
     if (!compute_layout(f->n, f->capacity, f->width, f->height, L)) return SS_ERR_INVALID_ARG;
-    if (L->pub.n_tiles > 65536) return SS_ERR_UNSUPPORTED;
+    if (L->pub.n_tiles > 65536 || L->pub.tiles_x > 256 || L->pub.tiles_y > 256) return SS_ERR_UNSUPPORTED;
     if (f->ws_bytes < L->pub.total_bytes) return SS_ERR_INVALID_ARG;
     return SS_OK;
 }

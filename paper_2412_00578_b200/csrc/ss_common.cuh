@@ -25,6 +25,7 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys per block tile
 constexpr int kEmitThreads = 256;                      // one Gaussian per thread
+constexpr int kInlineSpans = 4;                        // spans stored in the emission record
 constexpr int kDepthPasses = 4;                        // 32-bit depth keys, 8-bit digits
 
 // Look-back status words: 2-bit flag | 30-bit count.

@@ -29,6 +29,7 @@ __device__ __forceinline__ void edge_span(double lo, double hi, int tiles, int &
 // SnugBox (Sec. 4.1.1, Eqs. 15-16): exact bbox of a xd^2 + 2b xd yd + c yd^2 = t (Eq. 14);
 // half-extents sqrt(t c / D), sqrt(t a / D), D = ac - b^2.  Tangent points (R11).
 struct Snug {
+    double hx, hy;   // half-extents sqrt(t c / D), sqrt(t a / D)
     double xmin, xmax, ymin, ymax;
     double yl, yr;   // y of the x_min / x_max tangent points (B_l, B_r)
     double xt, xb;   // x of the y_min / y_max tangent points (B_t, B_b)
@@ -39,6 +40,8 @@ __device__ __forceinline__ Snug snugbox(double mx, double my, double a, double b
     double hx = sqrt(t * c / D);
     double hy = sqrt(t * a / D);
     Snug s;
+    s.hx = hx;
+    s.hy = hy;
     s.xmin = mx - hx;
     s.xmax = mx + hx;
     s.ymin = my - hy;
@@ -85,74 +88,96 @@ __device__ __forceinline__ void intersect_line(double m_free, double m_line, dou
 
 // AccuTile, Algorithm 1 along the shorter side of the SnugBox tile rect (R9),
 // the columns path by the a<->c / x<->y swap.  R10: a boundary line outside the
-// bbox yields the neutral pair (+inf, -inf).  Calls emit(tile_id) per tile; returns count.
-template <class Emit>
-__device__ __forceinline__ uint32_t accutile(double mx, double my, double a, double b, double c, double t,
-                                             int tiles_x, int tiles_y, Emit emit) {
-    Snug S = snugbox(mx, my, a, b, c, t);
-    int4 R = rect_of_snug(S, tiles_x, tiles_y);
-    if (R.x >= R.y || R.z >= R.w) return 0;
-    const bool rows = (R.w - R.z) <= (R.y - R.x);
-    double mf, ms, af, cs, ext_lo, ext_hi, smin, smax, tmin_s, tmax_s;
-    int s0, s1, f0, f1;
-    if (rows) {
-        mf = mx; ms = my; af = a; cs = c;
-        ext_lo = S.xmin; ext_hi = S.xmax; smin = S.ymin; smax = S.ymax;
-        tmin_s = S.yl; tmax_s = S.yr;
-        s0 = R.z; s1 = R.w; f0 = R.x; f1 = R.y;
+// bbox yields the neutral pair (+inf, -inf).
+struct Sweep {
+    bool rows;                                        // rows path (else columns)
+    double mf, ms, af, cs, b, t;                      // free/swept-axis centre and coefficients
+    double ext_lo, ext_hi, smin, smax, tmin_s, tmax_s;
+    int s0, s1, f0, f1;                               // swept lines [s0, s1), free span [f0, f1)
+};
+
+__device__ __forceinline__ bool accutile_setup_from(const Snug &S, const int4 &R, double mx, double my, double a,
+                                                    double b, double c, double t, Sweep &w) {
+    if (R.x >= R.y || R.z >= R.w) return false;
+    w.rows = (R.w - R.z) <= (R.y - R.x);
+    w.b = b;
+    w.t = t;
+    if (w.rows) {
+        w.mf = mx; w.ms = my; w.af = a; w.cs = c;
+        w.ext_lo = S.xmin; w.ext_hi = S.xmax; w.smin = S.ymin; w.smax = S.ymax;
+        w.tmin_s = S.yl; w.tmax_s = S.yr;
+        w.s0 = R.z; w.s1 = R.w; w.f0 = R.x; w.f1 = R.y;
     } else {
-        mf = my; ms = mx; af = c; cs = a;
-        ext_lo = S.ymin; ext_hi = S.ymax; smin = S.xmin; smax = S.xmax;
-        tmin_s = S.xt; tmax_s = S.xb;
-        s0 = R.x; s1 = R.y; f0 = R.z; f1 = R.w;
+        w.mf = my; w.ms = mx; w.af = c; w.cs = a;
+        w.ext_lo = S.ymin; w.ext_hi = S.ymax; w.smin = S.xmin; w.smax = S.xmax;
+        w.tmin_s = S.xt; w.tmax_s = S.xb;
+        w.s0 = R.x; w.s1 = R.y; w.f0 = R.z; w.f1 = R.w;
     }
+    return true;
+}
+
+__device__ __forceinline__ bool accutile_setup(double mx, double my, double a, double b, double c, double t,
+                                               int tiles_x, int tiles_y, Sweep &w) {
+    const Snug S = snugbox(mx, my, a, b, c, t);
+    const int4 R = rect_of_snug(S, tiles_x, tiles_y);
+    return accutile_setup_from(S, R, mx, my, a, b, c, t, w);
+}
+
+// Intersections(line, E) or the neutral pair when the algorithm does not compute it.
+__device__ __forceinline__ void sweep_line(const Sweep &w, double line, bool compute, double &lo, double &hi) {
+    lo = __longlong_as_double(0x7ff0000000000000ll);   // +inf
+    hi = __longlong_as_double(0xfff0000000000000ll);   // -inf
+    if (compute) intersect_line(w.mf, w.ms, w.af, w.b, w.cs, w.t, line, lo, hi);
+}
+
+// One row (or column) r of Algorithm 1 given i_min (its lower boundary line) and i_max (its
+// upper boundary line): e_min / e_max, Convert, clip to the rect.  Returns [tmin, tmax).
+__device__ __forceinline__ void sweep_row(const Sweep &w, int r, double imin_lo, double imin_hi, double imax_lo,
+                                          double imax_hi, int &tmin, int &tmax) {
+    const double lo_r = (double)(r * kTile), hi_r = (double)((r + 1) * kTile);
+    const double e_min = (w.tmin_s >= lo_r && w.tmin_s < hi_r) ? w.ext_lo : (imin_lo < imax_lo ? imin_lo : imax_lo);
+    const double e_max = (w.tmax_s >= lo_r && w.tmax_s < hi_r) ? w.ext_hi : (imin_hi > imax_hi ? imin_hi : imax_hi);
+    double g0 = floor(e_min / kTile), g1 = floor(e_max / kTile) + 1.0;
+    if (!(g0 > w.f0)) g0 = w.f0;
+    if (g0 > w.f1) g0 = w.f1;
+    if (!(g1 > w.f0)) g1 = w.f0;
+    if (g1 > w.f1) g1 = w.f1;
+    tmin = (int)g0;
+    tmax = (int)g1;
+}
+
+// Algorithm 1 in count mode on a prepared sweep (same loop as the sequential form below).
+// One span (row or column of the sweep) packed in 32 bits: first tile id (16 bits), length
+// (bits 16..24, <= 256), column-step flag (bit 31: consecutive tiles are tiles_x apart).
+__device__ __forceinline__ uint32_t pack_span(const Sweep &w, int r, int tmin, int tmax, int tiles_x) {
+    const uint32_t len = tmax > tmin ? (uint32_t)(tmax - tmin) : 0u;
+    const uint32_t first = len == 0 ? 0u : (w.rows ? (uint32_t)(r * tiles_x + tmin) : (uint32_t)(tmin * tiles_x + r));
+    return first | (len << 16) | (w.rows ? 0u : 0x80000000u);
+}
+
+// Algorithm 1 in count mode on a prepared sweep (the sequential loop, i_min <- i_max); the
+// first kInlineSpans spans are also returned packed (for the emission record).
+__device__ __forceinline__ uint32_t accutile_count(const Sweep &w, int tiles_x, uint32_t *spans) {
     uint32_t C = 0;
-    double imin_lo = __longlong_as_double(0x7ff0000000000000ll);   // +inf
-    double imin_hi = __longlong_as_double(0xfff0000000000000ll);   // -inf
-    double line_min = (double)(s0 * kTile);
-    if (line_min >= smin) intersect_line(mf, ms, af, b, cs, t, line_min, imin_lo, imin_hi);
-    for (int r = s0; r < s1; ++r) {
-        double imax_lo = __longlong_as_double(0x7ff0000000000000ll);
-        double imax_hi = __longlong_as_double(0xfff0000000000000ll);
-        double line_max = (double)((r + 1) * kTile);
-        if (line_max <= smax) intersect_line(mf, ms, af, b, cs, t, line_max, imax_lo, imax_hi);
-        double lo_r = (double)(r * kTile), hi_r = (double)((r + 1) * kTile);
-        double e_min = (tmin_s >= lo_r && tmin_s < hi_r) ? ext_lo : (imin_lo < imax_lo ? imin_lo : imax_lo);
-        double e_max = (tmax_s >= lo_r && tmax_s < hi_r) ? ext_hi : (imin_hi > imax_hi ? imin_hi : imax_hi);
-        double g0 = floor(e_min / kTile), g1 = floor(e_max / kTile) + 1.0;
-        if (!(g0 > f0)) g0 = f0;
-        if (g0 > f1) g0 = f1;
-        if (!(g1 > f0)) g1 = f0;
-        if (g1 > f1) g1 = f1;
-        const int tmin = (int)g0, tmax = (int)g1;
-        for (int k = tmin; k < tmax; ++k) emit(rows ? (uint32_t)(r * tiles_x + k) : (uint32_t)(k * tiles_x + r));
+    double imin_lo, imin_hi;
+    const double line_min = (double)(w.s0 * kTile);
+    sweep_line(w, line_min, line_min >= w.smin, imin_lo, imin_hi);
+    for (int r = w.s0; r < w.s1; ++r) {
+        double imax_lo, imax_hi;
+        const double line_max = (double)((r + 1) * kTile);
+        sweep_line(w, line_max, line_max <= w.smax, imax_lo, imax_hi);
+        int tmin, tmax;
+        sweep_row(w, r, imin_lo, imin_hi, imax_lo, imax_hi, tmin, tmax);
         if (tmax > tmin) C += (uint32_t)(tmax - tmin);
-        imin_lo = imax_lo;  // i_min <- i_max
+        const int j = r - w.s0;
+#pragma unroll
+        for (int q = 0; q < kInlineSpans; ++q)
+            if (j == q) spans[q] = pack_span(w, r, tmin, tmax, tiles_x);
+        imin_lo = imax_lo;
         imin_hi = imax_hi;
     }
     return C;
 }
-
-// Tile set of a stored record (count when emit is a no-op).  3-sigma / SnugBox: the rect.
-template <class Emit>
-__device__ __forceinline__ uint32_t tiles_of_record(int mode, float x, float y, float a, float b, float c,
-                                                    float sigma, int4 R, int tiles_x, int tiles_y, Emit emit) {
-    if (mode == SS_BIN_ACCUTILE) {
-        double t = 2.0 * log(255.0 * (double)sigma);  // Eq. 11 (R2)
-        return accutile((double)x, (double)y, (double)a, (double)b, (double)c, t, tiles_x, tiles_y, emit);
-    }
-    uint32_t C = 0;
-    for (int ty = R.z; ty < R.w; ++ty)
-        for (int tx = R.x; tx < R.y; ++tx) {
-            emit((uint32_t)(ty * tiles_x + tx));
-            ++C;
-        }
-    return C;
-}
-
-struct NoEmit {
-    __device__ __forceinline__ void operator()(uint32_t) const {}
-};
 
 // ---------------------------------------------------------------- SH basis (R13)
 template <int DEG>
@@ -184,10 +209,10 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *Y) {
 // One thread per Gaussian ("each thread processes a single Gaussian"), persistent
 // grid-stride loop so each CTA flushes its depth-digit histograms once.
 template <int DEG>
-__global__ void __launch_bounds__(256) k_preprocess(int n, const float4 *__restrict__ mean_opac,
+__global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__restrict__ mean_opac,
                                                     const float4 *__restrict__ scale, const float4 *__restrict__ rot,
                                                     const float4 *__restrict__ sh, CamArgs cam, int mode,
-                                                    float4 *__restrict__ rec, uint4 *__restrict__ bininfo,
+                                                    float4 *__restrict__ rec, uint4 *__restrict__ erec,
                                                     uint32_t *__restrict__ depth_key, uint32_t *__restrict__ hist,
                                                     uint32_t *__restrict__ n_visible) {
     __shared__ uint32_t s_hist[kDepthPasses][256];
@@ -207,10 +232,20 @@ __global__ void __launch_bounds__(256) k_preprocess(int n, const float4 *__restr
         float x2d = 0.f, y2d = 0.f, a = 0.f, b = 0.f, c = 0.f, rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;
         double td = 0.0;
         int4 R = make_int4(0, 0, 0, 0);
+        Snug snug;
+        snug.hx = snug.hy = 0.0;
+        uint32_t spans[kInlineSpans] = {0u, 0u, 0u, 0u};
+        uint32_t nspans = 0, cols = 0;
         if (pz >= cam.z_near) {
             const float tx = px / pz, ty = py / pz;
             x2d = cam.fx * tx + cam.cx;
             y2d = cam.fy * ty + cam.cy;
+            // likely visible: start pulling its SH planes into L2 now, so the colour loads
+            // after the (float64) tile count hit L2 instead of HBM
+            if (x2d > -0.25f * cam.W && x2d < 1.25f * cam.W && y2d > -0.25f * cam.H && y2d < 1.25f * cam.H) {
+#pragma unroll
+                for (int p = 0; p < NP; ++p) asm volatile("prefetch.global.L2 [%0];" ::"l"(sh + (size_t)p * n + i));
+            }
             float txc = tx, tyc = ty;
             if (cam.clip > 0.0f) {
                 const float limx = cam.clip * ((0.5f * (float)cam.W) / cam.fx);
@@ -264,13 +299,29 @@ __global__ void __launch_bounds__(256) k_preprocess(int n, const float4 *__restr
                 const double D = (double)a * (double)c - (double)b * (double)b;
                 td = 2.0 * log(255.0 * (double)mo.w);  // Eq. 11 (R2)
                 if (D > 0.0 && (mode == SS_BIN_3SIGMA || td > 0.0)) {
-                    if (mode == SS_BIN_3SIGMA)
+                    if (td > 0.0) snug = snugbox((double)x2d, (double)y2d, (double)a, (double)b, (double)c, td);
+                    if (mode == SS_BIN_3SIGMA) {
                         R = rect_3sigma((double)x2d, (double)y2d, (double)cxx, (double)cxy, (double)cyy, cam.tiles_x,
                                         cam.tiles_y);
-                    else
-                        R = rect_of_snug(snugbox((double)x2d, (double)y2d, (double)a, (double)b, (double)c, td),
-                                         cam.tiles_x, cam.tiles_y);
-                    count = tiles_of_record(mode, x2d, y2d, a, b, c, mo.w, R, cam.tiles_x, cam.tiles_y, NoEmit());
+                    } else {
+                        R = rect_of_snug(snug, cam.tiles_x, cam.tiles_y);
+                    }
+                    if (mode == SS_BIN_ACCUTILE) {
+                        Sweep w;
+                        if (accutile_setup_from(snug, R, (double)x2d, (double)y2d, (double)a, (double)b, (double)c,
+                                                td, w)) {
+                            count = accutile_count(w, cam.tiles_x, spans);
+                            nspans = (uint32_t)(w.s1 - w.s0);
+                            cols = w.rows ? 0u : 1u;
+                        }
+                    } else if (R.x < R.y && R.z < R.w) {
+                        count = (uint32_t)((R.y - R.x) * (R.w - R.z));
+                        nspans = (uint32_t)(R.w - R.z);
+#pragma unroll
+                        for (int q = 0; q < kInlineSpans; ++q)
+                            if (q < (int)nspans)
+                                spans[q] = (uint32_t)((R.z + q) * cam.tiles_x + R.x) | ((uint32_t)(R.y - R.x) << 16);
+                    }
                 }
             }
         }
@@ -302,18 +353,42 @@ __global__ void __launch_bounds__(256) k_preprocess(int n, const float4 *__restr
             rgb0 = acc0 > 0.0f ? acc0 : 0.0f;
             rgb1 = acc1 > 0.0f ? acc1 : 0.0f;
             rgb2 = acc2 > 0.0f ? acc2 : 0.0f;
-            rec[3 * (size_t)i + 0] = make_float4(x2d, y2d, a, b);
-            rec[3 * (size_t)i + 1] = make_float4(c, (float)td, mo.w, pz);
-            rec[3 * (size_t)i + 2] = make_float4(rgb0, rgb1, rgb2, 0.0f);
-            bininfo[i] = make_uint4((uint32_t)R.x | ((uint32_t)R.y << 16), (uint32_t)R.z | ((uint32_t)R.w << 16),
-                                    count, 0u);
+            // render-side culling box: SnugBox half-extents widened by the float32 error bound
+            // of the render's q (|dq| <= 16 eps cond(conic) q, cond <= (a+c)^2/D) + 1e-3 px
+            float hxr = 1e-3f, hyr = 1e-3f;
+            if (td > 0.0) {
+                const double ad = a, cd = c;
+                const double D = ad * cd - (double)b * (double)b;
+                const double widen = 1.0 + 16.0 * 5.9604644775390625e-08 * ((ad + cd) * (ad + cd) / D);
+                hxr = __double2float_ru(snug.hx * widen + 1e-3);
+                hyr = __double2float_ru(snug.hy * widen + 1e-3);
+            }
+            // render record (48 B): q0 (x, y, a, b) | q1 (c, t, sigma, hx) | q2 (hy, r, g, b)
+            float4 *q = rec + 3 * (size_t)i;
+            q[0] = make_float4(x2d, y2d, a, b);
+            q[1] = make_float4(c, (float)td, mo.w, hxr);
+            q[2] = make_float4(hyr, rgb0, rgb1, rgb2);
+            // emission record (32 B, one sector): e0 (count, info, span0, span1), e1 (span2, span3,
+            // aux0, aux1); info = nspans | inline flag << 8 | columns flag << 9; aux = t as float64
+            // bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1) for the fallback path.
+            uint32_t aux0, aux1;
+            if (mode == SS_BIN_ACCUTILE) {
+                aux0 = (uint32_t)__double2loint(td);
+                aux1 = (uint32_t)__double2hiint(td);
+            } else {
+                aux0 = (uint32_t)R.x | ((uint32_t)(R.y - R.x - 1) << 8) | ((uint32_t)R.z << 16) |
+                       ((uint32_t)(R.w - R.z - 1) << 24);
+                aux1 = 0u;
+            }
+            const uint32_t info = nspans | (nspans <= (uint32_t)kInlineSpans ? 0x100u : 0u) | (cols << 9);
+            erec[2 * (size_t)i + 0] = make_uint4(count, info, spans[0], spans[1]);
+            erec[2 * (size_t)i + 1] = make_uint4(spans[2], spans[3], aux0, aux1);
             const uint32_t key = __float_as_uint(pz);
             depth_key[i] = key;
 #pragma unroll
             for (int p = 0; p < kDepthPasses; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 0xFF], 1u);
             ++my_vis;
         } else {
-            bininfo[i] = make_uint4(0u, 0u, 0u, 0u);
             depth_key[i] = kNoTiles;
         }
     }
@@ -330,23 +405,93 @@ __global__ void __launch_bounds__(256) k_preprocess(int n, const float4 *__restr
 }
 
 // ---------------------------------------------------------------- a2+a3 emission kernel
-// Thread k handles the k-th visible Gaussian in (depth, index) order; its tile count is
-// exclusive-scanned across the grid with a decoupled look-back (block tickets assigned in
-// launch order), then its tiles are re-enumerated by tiles_of_record -- the very function
-// that produced the count -- and written at the offset.  A per-CTA tile histogram (shared
-// memory) feeds the tile sort and the ranges.
-__global__ void __launch_bounds__(kEmitThreads) k_emit(int mode, const float4 *__restrict__ rec,
-                                                       const uint4 *__restrict__ bininfo,
-                                                       const uint32_t *__restrict__ order,
-                                                       const uint32_t *__restrict__ n_visible, uint32_t cap,
-                                                       uint16_t *__restrict__ pair_tile,
-                                                       uint32_t *__restrict__ pair_value, uint32_t *tile_count,
-                                                       uint32_t *lookback, uint32_t *ticket, uint32_t *total_pairs,
-                                                       uint32_t *overflow, int tiles_x, int tiles_y, int n_tiles,
-                                                       int smem_hist) {
+// A CTA takes 256 consecutive visible Gaussians in (depth, index) order.
+//  1. Their tile counts are exclusive-scanned across the grid (block scan + decoupled
+//     look-back over block tickets assigned in launch order): the CTA's pairs occupy
+//     [base, base + total) in Gaussian order.
+//  2. Each thread runs the row (or column) loop of its Gaussian -- the same arithmetic as the
+//     count of a1 (AccuTile: Algorithm 1 with the i_min <- i_max carry; 3-sigma / SnugBox: the
+//     rect's rows) -- and stores one span (first tile, length, step, Gaussian) per row in
+//     shared memory.  At most kSpanCap spans per round; threads that do not fit go next round.
+//  3. The CTA flattens the spans (scan of lengths) and writes pair p of the round at
+//     base + round_base + p, so the global writes are contiguous and every thread writes the
+//     same number of pairs regardless of Gaussian size.  A per-CTA tile histogram in shared
+//     memory feeds the tile sort and the ranges.
+constexpr int kSpanCap = 2048;
+constexpr int kEmitBlock = kEmitThreads;
+
+// Warp-cooperative decoupled look-back: lane l inspects the status of CTA (bid - 1 - l - 32j);
+// the walk stops at the nearest inclusive prefix; aggregates before it are summed.  Returns
+// the exclusive prefix of CTA bid.  Called by one full warp.
+__device__ __forceinline__ uint32_t warp_lookback(const uint32_t *lookback, uint32_t bid, int lane) {
+    const volatile uint32_t *lb = lookback;
+    uint32_t acc = 0;
+    int base = (int)bid - 1;
+    for (;;) {
+        const int idx = base - lane;
+        uint32_t v;
+        int first_inc;
+        uint32_t need;
+        for (;;) {  // spin until every status up to the nearest inclusive one is published
+            v = idx >= 0 ? lb[idx] : kFlagInc;  // before CTA 0: a virtual inclusive 0
+            const uint32_t inc = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagInc);
+            const uint32_t zero = __ballot_sync(0xffffffffu, (v & ~kValMask) == 0);
+            first_inc = inc ? __ffs(inc) - 1 : 32;
+            need = first_inc == 32 ? 0xffffffffu : (0xffffffffu >> (31 - first_inc));
+            if (!(zero & need)) break;
+        }
+        uint32_t part = (lane <= first_inc) ? (v & kValMask) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        acc += part;
+        if (first_inc < 32) return acc;
+        base -= 32;
+    }
+}
+
+// Exclusive scan over the first 256 threads of a kEmitBlock CTA (the look-back warp passes 0
+// and ignores the result); every thread of the CTA must call it.
+__device__ __forceinline__ uint32_t emit_scan(uint32_t v, uint32_t *s_warp, uint32_t &total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31 && wid < 8) s_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t w = lane < 8 ? s_warp[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < 8) s_warp[lane] = w;
+    }
+    __syncthreads();
+    total = s_warp[7];
+    return (wid && wid < 8 ? s_warp[wid - 1] : 0u) + x - v;
+}
+
+__global__ void __launch_bounds__(kEmitBlock, 3) k_emit(int mode, const float4 *__restrict__ rec,
+                                                        const uint4 *__restrict__ erec,
+                                                        const uint32_t *__restrict__ order,
+                                                        const uint32_t *__restrict__ n_visible, uint32_t cap,
+                                                        uint16_t *__restrict__ pair_tile,
+                                                        uint32_t *__restrict__ pair_value, uint32_t *tile_count,
+                                                        uint32_t *lookback, uint32_t *ticket,
+                                                        uint32_t *total_pairs, uint32_t *overflow, int tiles_x,
+                                                        int tiles_y, int n_tiles, int smem_hist) {
     extern __shared__ uint32_t s_tile_hist[];
+    __shared__ uint32_t s_span[kSpanCap];  // first tile | len << 16 | column-step flag << 31
+    __shared__ uint32_t s_gid[kSpanCap];
+    __shared__ uint32_t s_pfx[kSpanCap];   // exclusive prefix of span lengths within the round
     __shared__ uint32_t s_warp[8];
-    __shared__ uint32_t s_bid, s_base;
+    __shared__ uint32_t s_bid, s_base, s_total, s_nspans;
+    const bool lb_warp = threadIdx.x >= kEmitThreads;
+    const int lane = threadIdx.x & 31;
     for (int t = threadIdx.x; t < (smem_hist ? n_tiles : 0); t += blockDim.x) s_tile_hist[t] = 0;
     const uint32_t nv = *n_visible;
     uint32_t *hist = smem_hist ? s_tile_hist : tile_count;
@@ -358,57 +503,131 @@ __global__ void __launch_bounds__(kEmitThreads) k_emit(int mode, const float4 *_
         if ((size_t)bid * kEmitThreads >= nv) break;
         const uint32_t k = bid * kEmitThreads + threadIdx.x;
         uint32_t g = 0, cnt = 0;
-        uint4 bi = make_uint4(0, 0, 0, 0);
-        if (k < nv) {
+        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;
+        if (!lb_warp && k < nv) {
             g = order[k];
-            bi = bininfo[g];
-            cnt = bi.z;
+            e0 = erec[2 * (size_t)g + 0];  // one aligned 32 B sector per Gaussian
+            e1 = erec[2 * (size_t)g + 1];
+            cnt = e0.x;
         }
         uint32_t total;
-        const uint32_t excl = block_exclusive_scan_256(cnt, s_warp, total);
-        if (threadIdx.x == 0) {
-            // decoupled look-back over the preceding CTAs' published sums
-            volatile uint32_t *lb = lookback;
-            if (bid == 0) {
-                lb[0] = kFlagInc | total;
-                s_base = 0;
-            } else {
-                lb[bid] = kFlagAgg | total;
-                uint32_t acc = 0;
-                int p = (int)bid - 1;
-                for (;;) {
-                    uint32_t v;
-                    do { v = lb[p]; } while ((v & ~kValMask) == 0);
-                    acc += v & kValMask;
-                    if ((v & ~kValMask) == kFlagInc) break;
-                    --p;
+        emit_scan(cnt, s_warp, total);
+        const uint32_t ns = cnt ? (e0.y & 0xFFu) : 0u;
+        const bool inline_spans = (e0.y & 0x100u) != 0;
+        if (threadIdx.x == 0) lookback[bid] = (bid == 0 ? kFlagInc : kFlagAgg) | total;
+        bool first_round = true;
+        // warp 0: decoupled look-back (run after its span generation, so that predecessors have
+        // had time to publish), the inclusive prefix, and P for the last CTA
+        auto emit_lookback_publish = [&]() {
+            const uint32_t acc = bid == 0 ? 0u : warp_lookback(lookback, bid, lane);
+            if (lane == 0) {
+                if (bid > 0) {
+                    volatile uint32_t *lbv = lookback;
+                    lbv[bid] = kFlagInc | (acc + total);
                 }
-                lb[bid] = kFlagInc | (acc + total);
                 s_base = acc;
+                if ((bid + 1) * kEmitThreads >= nv) {
+                    *total_pairs = acc + total;
+                    *overflow = acc + total > cap ? 1u : 0u;
+                }
             }
-            if ((bid + 1) * kEmitThreads >= nv) {  // the CTA holding the last visible Gaussian
-                const uint32_t P = s_base + total;
-                *total_pairs = P;
-                *overflow = P > cap ? 1u : 0u;
+        };
+        bool pending = ns > 0;
+        uint32_t round_base = 0;  // pairs of this CTA written in previous rounds
+        while (__syncthreads_or(pending)) {
+            uint32_t span_tot;
+            const uint32_t sofs = emit_scan(pending ? ns : 0u, s_warp, span_tot);
+            const bool take = pending && sofs + ns <= (uint32_t)kSpanCap;
+            // spans taken this round: all, or up to the first thread that does not fit
+            if (threadIdx.x == 0 && span_tot <= (uint32_t)kSpanCap) s_nspans = span_tot;
+            if (pending && sofs <= (uint32_t)kSpanCap && sofs + ns > (uint32_t)kSpanCap) s_nspans = sofs;
+            if (take) {
+                uint32_t j = sofs;
+                if (inline_spans) {  // spans recorded by ss_preprocess's count
+                    const uint32_t sp[kInlineSpans] = {e0.z, e0.w, e1.x, e1.y};
+#pragma unroll
+                    for (int q = 0; q < kInlineSpans; ++q)
+                        if (q < (int)ns) {
+                            s_span[j + q] = sp[q];
+                            s_gid[j + q] = g;
+                        }
+                } else if (mode == SS_BIN_ACCUTILE) {  // rare: more rows than inline slots
+                    const float4 q0 = rec[3 * (size_t)g + 0];
+                    const float c = rec[3 * (size_t)g + 1].x;
+                    const double t = __hiloint2double((int)e1.w, (int)e1.z);
+                    Sweep w;
+                    accutile_setup((double)q0.x, (double)q0.y, (double)q0.z, (double)q0.w, (double)c, t, tiles_x,
+                                   tiles_y, w);
+                    double imin_lo, imin_hi;
+                    const double line_min = (double)(w.s0 * kTile);
+                    sweep_line(w, line_min, line_min >= w.smin, imin_lo, imin_hi);
+                    for (int r = w.s0; r < w.s1; ++r, ++j) {
+                        double imax_lo, imax_hi;
+                        const double line_max = (double)((r + 1) * kTile);
+                        sweep_line(w, line_max, line_max <= w.smax, imax_lo, imax_hi);
+                        int tmin, tmax;
+                        sweep_row(w, r, imin_lo, imin_hi, imax_lo, imax_hi, tmin, tmax);
+                        s_span[j] = pack_span(w, r, tmin, tmax, tiles_x);
+                        s_gid[j] = g;
+                        imin_lo = imax_lo;  // i_min <- i_max
+                        imin_hi = imax_hi;
+                    }
+                } else {  // 3-sigma / SnugBox: the rect's rows
+                    const uint32_t pr = e1.z;
+                    const int x0 = (int)(pr & 0xFF), w_ = (int)((pr >> 8) & 0xFF) + 1, y0 = (int)((pr >> 16) & 0xFF);
+                    for (int r = y0; r < y0 + (int)ns; ++r, ++j) {
+                        s_span[j] = (uint32_t)(r * tiles_x + x0) | ((uint32_t)w_ << 16);
+                        s_gid[j] = g;
+                    }
+                }
+                pending = false;
             }
-        }
-        __syncthreads();
-        if (cnt) {
-            const uint32_t off = s_base + excl;
-            const float4 r0 = rec[3 * (size_t)g + 0];
-            const float4 r1 = rec[3 * (size_t)g + 1];
-            const int4 R = make_int4((int)(bi.x & 0xFFFF), (int)(bi.x >> 16), (int)(bi.y & 0xFFFF), (int)(bi.y >> 16));
-            uint32_t j = 0;
-            tiles_of_record(mode, r0.x, r0.y, r0.z, r0.w, r1.x, r1.z, R, tiles_x, tiles_y, [&](uint32_t tile) {
-                const uint32_t o = off + j;
+            if (first_round && threadIdx.x < 32) emit_lookback_publish();
+            first_round = false;
+            __syncthreads();
+            const uint32_t nspans = s_nspans;
+            // exclusive prefix of the span lengths (8 spans per thread of the first 256)
+            uint32_t loc[kSpanCap / kEmitThreads];
+            uint32_t my = 0;
+#pragma unroll
+            for (int q = 0; q < kSpanCap / kEmitThreads; ++q) {
+                const uint32_t jj = threadIdx.x * (kSpanCap / kEmitThreads) + q;
+                loc[q] = (!lb_warp && jj < nspans) ? (s_span[jj] >> 16) & 0x7FFFu : 0u;
+                my += loc[q];
+            }
+            uint32_t round_pairs;
+            uint32_t run = emit_scan(my, s_warp, round_pairs);
+            if (!lb_warp) {
+#pragma unroll
+                for (int q = 0; q < kSpanCap / kEmitThreads; ++q) {
+                    const uint32_t jj = threadIdx.x * (kSpanCap / kEmitThreads) + q;
+                    if (jj < nspans) s_pfx[jj] = run;
+                    run += loc[q];
+                }
+            }
+            __syncthreads();
+            // flatten (all kEmitBlock threads): pair p of the round -> last span j with s_pfx[j] <= p
+            const uint32_t out0 = s_base + round_base;
+            for (uint32_t p = threadIdx.x; p < round_pairs; p += kEmitBlock) {
+                uint32_t lo = 0, hi = nspans - 1;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi + 1) >> 1;
+                    if (s_pfx[mid] <= p) lo = mid;
+                    else hi = mid - 1;
+                }
+                const uint32_t sp = s_span[lo];
+                const uint32_t step = (sp & 0x80000000u) ? (uint32_t)tiles_x : 1u;
+                const uint32_t tile = (sp & 0xFFFFu) + (p - s_pfx[lo]) * step;
+                const uint32_t o = out0 + p;
                 if (o < cap) {
                     pair_tile[o] = (uint16_t)tile;
-                    pair_value[o] = g;
+                    pair_value[o] = s_gid[lo];
                 }
                 atomicAdd(hist + tile, 1u);
-                ++j;
-            });
+            }
+            round_base += round_pairs;
         }
+        if (first_round && threadIdx.x < 32) emit_lookback_publish();  // CTA without spans
     }
     if (smem_hist) {
         __syncthreads();
@@ -433,7 +652,7 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
 #define SS_PRE_ARGS                                                                                       \
     sc.n, reinterpret_cast<const float4 *>(sc.mean_opac), reinterpret_cast<const float4 *>(sc.scale),         \
         reinterpret_cast<const float4 *>(sc.rot), reinterpret_cast<const float4 *>(sc.sh), cam, mode,         \
-        at<float4>(ws, P.rec), at<uint4>(ws, P.bininfo), at<uint32_t>(ws, P.depth_key),                      \
+        at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key),                         \
         at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible)
     switch (sc.sh_degree) {
         case 0: k_preprocess<0><<<grid, 256, 0, st>>>(SS_PRE_ARGS); break;
@@ -453,10 +672,10 @@ cudaError_t launch_emit(const CamArgs &cam, int mode, void *ws, const Layout &L,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int smem_hist = P.n_tiles <= 12288 ? 1 : 0;
     const size_t smem = smem_hist ? (size_t)P.n_tiles * 4 : 0;
-    if (smem > 48 * 1024) cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = (int)L.nblk_emit < sms * 4 ? (int)L.nblk_emit : sms * 4;
-    k_emit<<<grid, kEmitThreads, smem, st>>>(
-        mode, at<const float4>(ws, P.rec), at<const uint4>(ws, P.bininfo), at<const uint32_t>(ws, P.order),
+    k_emit<<<grid, kEmitBlock, smem, st>>>(
+        mode, at<const float4>(ws, P.rec), at<const uint4>(ws, P.erec), at<const uint32_t>(ws, P.order),
         at<const uint32_t>(ws, P.n_visible), L.capacity,
         at<uint16_t>(ws, P.pair_tile), at<uint32_t>(ws, P.pair_value), at<uint32_t>(ws, P.tile_count),
         at<uint32_t>(ws, L.lb_emit), at<uint32_t>(ws, L.counters) + 8, at<uint32_t>(ws, P.total_pairs),

@@ -16,10 +16,12 @@ namespace {
 
 constexpr int kBatch = 256;
 
-struct __align__(16) GRec {
-    float x, y, a, b2;      // b2 = 2b (exact)
-    float c, t, sigma, pad;
-    float r, g, b, pad2;
+// Shared-memory batch of gathered records, split by use: the per-warp culling box, the conic
+// (skip test), the colour.
+struct Batch {
+    float4 box[kBatch];  // x, y, hx, hy  (hx, hy: conservative alpha >= 1/255 half-extents)
+    float4 con[kBatch];  // a, 2b, c, t
+    float4 col[kBatch];  // r, g, b, sigma
 };
 
 __device__ __forceinline__ float pixel_q(float fx, float fy, float x, float y, float a, float b2, float c) {
@@ -36,65 +38,116 @@ __device__ __forceinline__ float alpha_of(float q, float sigma) {
     return fminf(0.99f, sigma * e);
 }
 
-__device__ __forceinline__ void load_batch(GRec *s, const uint32_t *__restrict__ vals, const float4 *__restrict__ rec,
-                                           uint32_t j, uint32_t end, uint32_t *s_id) {
+__device__ __forceinline__ void load_batch(Batch &s, const uint32_t *__restrict__ vals,
+                                           const float4 *__restrict__ rec, uint32_t j, uint32_t end,
+                                           uint32_t *s_id) {
     if (j < end) {
         const uint32_t g = vals[j];
-        const float4 r0 = __ldg(rec + 3 * (size_t)g + 0);
-        const float4 r1 = __ldg(rec + 3 * (size_t)g + 1);
-        const float4 r2 = __ldg(rec + 3 * (size_t)g + 2);
-        GRec &d = s[threadIdx.x];
-        d.x = r0.x; d.y = r0.y; d.a = r0.z; d.b2 = r0.w + r0.w;
-        d.c = r1.x; d.t = r1.y; d.sigma = r1.z; d.pad = 0.f;
-        d.r = r2.x; d.g = r2.y; d.b = r2.z; d.pad2 = 0.f;
+        const float4 q0 = __ldg(rec + 3 * (size_t)g + 0);  // x, y, a, b
+        const float4 q1 = __ldg(rec + 3 * (size_t)g + 1);  // c, t, sigma, hx
+        const float4 q2 = __ldg(rec + 3 * (size_t)g + 2);  // hy, r, g, b
+        s.box[threadIdx.x] = make_float4(q0.x, q0.y, q1.w, q2.x);
+        s.con[threadIdx.x] = make_float4(q0.z, q0.w + q0.w, q1.x, q1.y);
+        s.col[threadIdx.x] = make_float4(q2.y, q2.z, q2.w, q1.z);
         if (s_id) s_id[threadIdx.x] = g;
     }
+}
+
+// Pixel p (0..255) of a tile is (p & 15, p >> 4) in the tile, row-major.
+__device__ __forceinline__ void tile_pixel(int tile, int tiles_x, int p, int &px, int &py) {
+    px = (tile % tiles_x) * kTile + (p & 15);
+    py = (tile / tiles_x) * kTile + (p >> 4);
+}
+
+// Per-pixel state kept in shared memory between batches, so that before every batch the
+// still-active pixels can be compacted onto the lowest threads: warps whose pixels have all
+// terminated stop issuing, instead of idling lane by lane inside partially-done warps
+// (the per-pixel walk and its arithmetic are unchanged).
+struct PixState {
+    float T[256], C0[256], C1[256], C2[256];
+    uint32_t last[256];
+    uint8_t done[256];
+    uint16_t list[256];
+};
+
+// Compacts the active pixels (one flag per thread = pixel threadIdx.x) into st.list; returns
+// their number.  Every thread of the CTA must call it.
+__device__ __forceinline__ uint32_t compact_active(bool active, PixState &st, uint32_t *s_warp) {
+    uint32_t n_active;
+    const uint32_t pos = block_exclusive_scan_256(active ? 1u : 0u, s_warp, n_active);
+    if (active) st.list[pos] = (uint16_t)threadIdx.x;
+    __syncthreads();
+    return n_active;
 }
 
 __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
                                                 const float4 *__restrict__ rec, int W, int H, int tiles_x, float bg0,
                                                 float bg1, float bg2, float *__restrict__ out_rgb,
                                                 float *__restrict__ out_T, uint32_t *__restrict__ out_nc) {
-    __shared__ GRec s_g[kBatch];
+    __shared__ Batch s;
+    __shared__ PixState st;
+    __shared__ uint32_t s_warp[8];
     const int tile = blockIdx.x;
-    const int px = (tile % tiles_x) * kTile + (threadIdx.x & 15);
-    const int py = (tile / tiles_x) * kTile + (threadIdx.x >> 4);
-    const bool inside = px < W && py < H;
-    const float fpx = (float)px, fpy = (float)py;
+    int mpx, mpy;
+    tile_pixel(tile, tiles_x, threadIdx.x, mpx, mpy);
+    const bool inside = mpx < W && mpy < H;
     const uint2 range = ranges[tile];
-    bool done = !inside;
-    float T = 1.0f, C0 = 0.f, C1 = 0.f, C2 = 0.f;
-    uint32_t last = 0;
+    st.T[threadIdx.x] = 1.0f;
+    st.C0[threadIdx.x] = st.C1[threadIdx.x] = st.C2[threadIdx.x] = 0.0f;
+    st.last[threadIdx.x] = 0;
+    st.done[threadIdx.x] = inside ? 0 : 1;
     for (uint32_t start = range.x; start < range.y; start += kBatch) {
-        if (__syncthreads_count(done) == blockDim.x) break;
-        load_batch(s_g, vals, rec, start + threadIdx.x, range.y, nullptr);
         __syncthreads();
-        const int cnt = min((uint32_t)kBatch, range.y - start);
-        for (int k = 0; k < cnt && !done; ++k) {
-            const GRec &g = s_g[k];
-            const float q = pixel_q(fpx, fpy, g.x, g.y, g.a, g.b2, g.c);
-            if (!(q <= g.t)) continue;  // alpha < 1/255: no contribution (Eq. 9, R15)
-            const float alpha = alpha_of(q, g.sigma);
-            const float Tn = T * (1.0f - alpha);
-            if (Tn < 1e-4f) {  // R16: stop before blending
-                done = true;
-                break;
+        const uint32_t n_active = compact_active(!st.done[threadIdx.x], st, s_warp);
+        if (n_active == 0) break;
+        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr);
+        __syncthreads();
+        if (threadIdx.x < n_active) {
+            const int pp = st.list[threadIdx.x];
+            int px, py;
+            tile_pixel(tile, tiles_x, pp, px, py);
+            const float fpx = (float)px, fpy = (float)py;
+            float T = st.T[pp], C0 = st.C0[pp], C1 = st.C1[pp], C2 = st.C2[pp];
+            uint32_t last = st.last[pp];
+            bool done = false;
+            const int cnt = min((uint32_t)kBatch, range.y - start);
+            for (int k = 0; k < cnt; ++k) {
+                const float4 bx = s.box[k];
+                const float4 cn = s.con[k];
+                const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
+                if (!(q <= cn.w)) continue;  // alpha < 1/255: no contribution (Eq. 9, R15)
+                const float4 cl = s.col[k];
+                const float alpha = alpha_of(q, cl.w);
+                const float Tn = T * (1.0f - alpha);
+                if (Tn < 1e-4f) {  // R16: stop before blending
+                    done = true;
+                    break;
+                }
+                const float w = alpha * T;
+                C0 = fmaf(cl.x, w, C0);
+                C1 = fmaf(cl.y, w, C1);
+                C2 = fmaf(cl.z, w, C2);
+                T = Tn;
+                last = start - range.x + k + 1;
             }
-            const float w = alpha * T;
-            C0 = fmaf(g.r, w, C0);
-            C1 = fmaf(g.g, w, C1);
-            C2 = fmaf(g.b, w, C2);
-            T = Tn;
-            last = start - range.x + k + 1;
+            st.T[pp] = T;
+            st.C0[pp] = C0;
+            st.C1[pp] = C1;
+            st.C2[pp] = C2;
+            st.last[pp] = last;
+            st.done[pp] = done ? 1 : 0;
         }
     }
+    __syncthreads();
     if (inside) {
-        const size_t p = (size_t)py * W + px, plane = (size_t)W * H;
-        out_rgb[p] = fmaf(T, bg0, C0);
-        out_rgb[plane + p] = fmaf(T, bg1, C1);
-        out_rgb[2 * plane + p] = fmaf(T, bg2, C2);
+        const int p0 = threadIdx.x;
+        const float T = st.T[p0];
+        const size_t p = (size_t)mpy * W + mpx, plane = (size_t)W * H;
+        out_rgb[p] = fmaf(T, bg0, st.C0[p0]);
+        out_rgb[plane + p] = fmaf(T, bg1, st.C1[p0]);
+        out_rgb[2 * plane + p] = fmaf(T, bg2, st.C2[p0]);
         if (out_T) out_T[p] = T;
-        if (out_nc) out_nc[p] = last;
+        if (out_nc) out_nc[p] = st.last[p0];
     }
 }
 
@@ -102,91 +155,130 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
 // recovering T_i = T_{i+1} / (1 - alpha_i) and the suffix colour S <- alpha c + (1-alpha) S:
 //   dC_ch/dalpha_i = T_i (c_ch - S_ch) - T_final bg_ch / (1 - alpha_i)      (from Eq. 7)
 //   U_i += sum_ch (sigma_i dC_ch/dalpha_i)^2                                 (Eqs. 20-21)
-// Per batch, per-Gaussian sums are reduced warp -> CTA in shared memory and added to the
-// float64 score with one atomic per (tile, Gaussian).
+// Both walks compact the active pixels per batch like k_render.  Per batch, per-Gaussian
+// sums are reduced warp -> CTA in shared memory and added to the float64 score with one
+// atomic per (tile, Gaussian).
 __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ ranges,
                                                      const uint32_t *__restrict__ vals,
                                                      const float4 *__restrict__ rec, int W, int H, int tiles_x,
                                                      float bg0, float bg1, float bg2, double *__restrict__ score) {
-    __shared__ GRec s_g[kBatch];
+    __shared__ Batch s;
+    __shared__ PixState st;  // forward: T, last, done; backward: T (running), C0..2 = suffix S
+    __shared__ float s_Tfin[256];
     __shared__ uint32_t s_id[kBatch];
     __shared__ float s_part[8][kBatch];
+    __shared__ uint32_t s_warp[8];
     __shared__ uint32_t s_max;
     const int tile = blockIdx.x;
-    const int px = (tile % tiles_x) * kTile + (threadIdx.x & 15);
-    const int py = (tile / tiles_x) * kTile + (threadIdx.x >> 4);
-    const bool inside = px < W && py < H;
-    const float fpx = (float)px, fpy = (float)py;
+    int mpx, mpy;
+    tile_pixel(tile, tiles_x, threadIdx.x, mpx, mpy);
+    const bool inside = mpx < W && mpy < H;
     const uint2 range = ranges[tile];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    bool done = !inside;
-    float T = 1.0f;
-    uint32_t last = 0;
+    st.T[threadIdx.x] = 1.0f;
+    st.last[threadIdx.x] = 0;
+    st.done[threadIdx.x] = inside ? 0 : 1;
     if (threadIdx.x == 0) s_max = 0;
     // forward
     for (uint32_t start = range.x; start < range.y; start += kBatch) {
-        if (__syncthreads_count(done) == blockDim.x) break;
-        load_batch(s_g, vals, rec, start + threadIdx.x, range.y, nullptr);
         __syncthreads();
-        const int cnt = min((uint32_t)kBatch, range.y - start);
-        for (int k = 0; k < cnt && !done; ++k) {
-            const GRec &g = s_g[k];
-            const float q = pixel_q(fpx, fpy, g.x, g.y, g.a, g.b2, g.c);
-            if (!(q <= g.t)) continue;
-            const float alpha = alpha_of(q, g.sigma);
-            const float Tn = T * (1.0f - alpha);
-            if (Tn < 1e-4f) {
-                done = true;
-                break;
+        const uint32_t n_active = compact_active(!st.done[threadIdx.x], st, s_warp);
+        if (n_active == 0) break;
+        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr);
+        __syncthreads();
+        if (threadIdx.x < n_active) {
+            const int pp = st.list[threadIdx.x];
+            int px, py;
+            tile_pixel(tile, tiles_x, pp, px, py);
+            const float fpx = (float)px, fpy = (float)py;
+            float T = st.T[pp];
+            uint32_t last = st.last[pp];
+            bool done = false;
+            const int cnt = min((uint32_t)kBatch, range.y - start);
+            for (int k = 0; k < cnt; ++k) {
+                const float4 bx = s.box[k];
+                const float4 cn = s.con[k];
+                const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
+                if (!(q <= cn.w)) continue;
+                const float alpha = alpha_of(q, s.col[k].w);
+                const float Tn = T * (1.0f - alpha);
+                if (Tn < 1e-4f) {
+                    done = true;
+                    break;
+                }
+                T = Tn;
+                last = start - range.x + k + 1;
             }
-            T = Tn;
-            last = start - range.x + k + 1;
+            st.T[pp] = T;
+            st.last[pp] = last;
+            st.done[pp] = done ? 1 : 0;
         }
     }
     __syncthreads();
-    atomicMax(&s_max, last);
+    const uint32_t my_last = st.last[threadIdx.x];
+    atomicMax(&s_max, my_last);
+    s_Tfin[threadIdx.x] = st.T[threadIdx.x];
+    st.C0[threadIdx.x] = st.C1[threadIdx.x] = st.C2[threadIdx.x] = 0.0f;
     __syncthreads();
     const uint32_t max_last = s_max;
-    const float Tfin = T;
-    float S0 = 0.f, S1 = 0.f, S2 = 0.f;
-    // backward, batches from the end
+    // backward, batches from the end; a pixel is active in [start, end) iff last > start
     for (uint32_t end = range.x + max_last; end > range.x;) {
         const uint32_t start = end - range.x > (uint32_t)kBatch ? end - kBatch : range.x;
         const int cnt = (int)(end - start);
         __syncthreads();
-        load_batch(s_g, vals, rec, start + threadIdx.x, end, s_id);
+        const uint32_t n_active = compact_active(my_last > start - range.x, st, s_warp);
+        load_batch(s, vals, rec, start + threadIdx.x, end, s_id);
         __syncthreads();
-        for (int k = cnt - 1; k >= 0; --k) {
-            const GRec &g = s_g[k];
-            float term = 0.f;
-            if (start - range.x + (uint32_t)k < last) {
-                const float q = pixel_q(fpx, fpy, g.x, g.y, g.a, g.b2, g.c);
-                if (q <= g.t) {
-                    const float alpha = alpha_of(q, g.sigma);
-                    const float om = 1.0f - alpha;
-                    T = T / om;
-                    const float bgs = Tfin / om;
-                    const float d0 = T * (g.r - S0) - bgs * bg0;
-                    const float d1 = T * (g.g - S1) - bgs * bg1;
-                    const float d2 = T * (g.b - S2) - bgs * bg2;
-                    term = g.sigma * g.sigma * (d0 * d0 + d1 * d1 + d2 * d2);
-                    S0 = alpha * g.r + om * S0;
-                    S1 = alpha * g.g + om * S1;
-                    S2 = alpha * g.b + om * S2;
+        const uint32_t n_warps = (n_active + 31) / 32;
+        if ((uint32_t)warp < n_warps) {
+            const bool act = threadIdx.x < n_active;
+            const int pp = act ? st.list[threadIdx.x] : 0;
+            int px, py;
+            tile_pixel(tile, tiles_x, pp, px, py);
+            const float fpx = (float)px, fpy = (float)py;
+            const uint32_t plast = act ? st.last[pp] : 0u;
+            const float Tfin = s_Tfin[pp];
+            float T = act ? st.T[pp] : 1.0f;
+            float S0 = st.C0[pp], S1 = st.C1[pp], S2 = st.C2[pp];
+            for (int k = cnt - 1; k >= 0; --k) {
+                float term = 0.f;
+                if (start - range.x + (uint32_t)k < plast) {
+                    const float4 bx = s.box[k];
+                    const float4 cn = s.con[k];
+                    const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
+                    if (q <= cn.w) {
+                        const float4 cl = s.col[k];
+                        const float alpha = alpha_of(q, cl.w);
+                        const float om = 1.0f - alpha;
+                        T = T / om;
+                        const float bgs = Tfin / om;
+                        const float d0 = T * (cl.x - S0) - bgs * bg0;
+                        const float d1 = T * (cl.y - S1) - bgs * bg1;
+                        const float d2 = T * (cl.z - S2) - bgs * bg2;
+                        term = cl.w * cl.w * (d0 * d0 + d1 * d1 + d2 * d2);
+                        S0 = alpha * cl.x + om * S0;
+                        S1 = alpha * cl.y + om * S1;
+                        S2 = alpha * cl.z + om * S2;
+                    }
                 }
-            }
-            if (__any_sync(0xffffffffu, term != 0.f)) {
+                if (__any_sync(0xffffffffu, term != 0.f)) {
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+                    for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+                }
+                if (lane == 0) s_part[warp][k] = term;
             }
-            if (lane == 0) s_part[warp][k] = term;
+            if (act) {
+                st.T[pp] = T;
+                st.C0[pp] = S0;
+                st.C1[pp] = S1;
+                st.C2[pp] = S2;
+            }
         }
         __syncthreads();
         if ((int)threadIdx.x < cnt) {
-            float s = 0.f;
-#pragma unroll
-            for (int w = 0; w < 8; ++w) s += s_part[w][threadIdx.x];
-            if (s != 0.f) atomicAdd(score + s_id[threadIdx.x], (double)s);
+            float sum = 0.f;
+            for (uint32_t w = 0; w < n_warps; ++w) sum += s_part[w][threadIdx.x];
+            if (sum != 0.f) atomicAdd(score + s_id[threadIdx.x], (double)sum);
         }
         end = start;
     }
@@ -194,35 +286,39 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
 
 // Measurement only (not on the timed path): the render's work counts for one frame, from
 // the same per-pixel walk as k_render.  counters[0] += E_pix (evaluations each pixel makes
-// until it terminates), [1] += E_blend (evaluations that blend), [2] += E_cta (evaluations a
-// CTA issues in lock-step until its last pixel terminates: 256 x Gaussians staged),
-// [3] += pixels.
+// until it terminates, the method's work), [1] += E_blend (evaluations that blend),
+// [2] += E_cta (evaluations a CTA issues in lock-step until its last pixel terminates:
+// 256 x Gaussians staged), [3] += pixels, [4] += evaluations left after per-warp culling.
 __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ ranges,
                                                       const uint32_t *__restrict__ vals,
                                                       const float4 *__restrict__ rec, int W, int H, int tiles_x,
                                                       unsigned long long *counters) {
-    __shared__ GRec s_g[kBatch];
+    __shared__ Batch s;
+    __shared__ unsigned long long s_acc[5];
     const int tile = blockIdx.x;
-    const int px = (tile % tiles_x) * kTile + (threadIdx.x & 15);
-    const int py = (tile / tiles_x) * kTile + (threadIdx.x >> 4);
+    int px, py;
+    tile_pixel(tile, tiles_x, threadIdx.x, px, py);
     const bool inside = px < W && py < H;
     const float fpx = (float)px, fpy = (float)py;
     const uint2 range = ranges[tile];
     bool done = !inside;
     float T = 1.0f;
-    unsigned long long e_pix = 0, e_blend = 0, e_cta = 0;
+    unsigned long long e_pix = 0, e_blend = 0, e_cta = 0, e_warp = 0;
+    if (threadIdx.x < 5) s_acc[threadIdx.x] = 0;
     for (uint32_t start = range.x; start < range.y; start += kBatch) {
         if (__syncthreads_count(done) == blockDim.x) break;
-        load_batch(s_g, vals, rec, start + threadIdx.x, range.y, nullptr);
+        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr);
         __syncthreads();
         const int cnt = min((uint32_t)kBatch, range.y - start);
         e_cta += cnt;
+        // compacted warps: ceil(active / 32) warps walk until their last pixel terminates
         for (int k = 0; k < cnt && !done; ++k) {
-            const GRec &g = s_g[k];
             ++e_pix;
-            const float q = pixel_q(fpx, fpy, g.x, g.y, g.a, g.b2, g.c);
-            if (!(q <= g.t)) continue;
-            const float alpha = alpha_of(q, g.sigma);
+            const float4 bx = s.box[k];
+            const float4 cn = s.con[k];
+            const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
+            if (!(q <= cn.w)) continue;
+            const float alpha = alpha_of(q, s.col[k].w);
             const float Tn = T * (1.0f - alpha);
             if (Tn < 1e-4f) {
                 done = true;
@@ -232,10 +328,25 @@ __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ 
             T = Tn;
         }
     }
-    atomicAdd(counters + 0, e_pix);
-    atomicAdd(counters + 1, e_blend);
-    if (threadIdx.x == 0) atomicAdd(counters + 2, e_cta * blockDim.x);
-    if (inside) atomicAdd(counters + 3, 1ull);
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        e_pix += __shfl_xor_sync(0xffffffffu, e_pix, o);
+        e_blend += __shfl_xor_sync(0xffffffffu, e_blend, o);
+    }
+    const unsigned n_inside = __syncthreads_count(inside);
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&s_acc[0], e_pix);
+        atomicAdd(&s_acc[1], e_blend);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        atomicAdd(counters + 0, s_acc[0]);
+        atomicAdd(counters + 1, s_acc[1]);
+        atomicAdd(counters + 2, e_cta * blockDim.x);
+        atomicAdd(counters + 3, (unsigned long long)n_inside);
+        atomicAdd(counters + 4, e_warp);
+    }
 }
 
 }  // namespace

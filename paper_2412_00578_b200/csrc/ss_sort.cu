@@ -29,12 +29,13 @@ __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
 //  3. digit totals -> look-back publication (aggregate, then inclusive prefix);
 //  4. scatter into shared memory in tile-sorted order, then write out contiguous digit runs.
 template <typename K, bool IMPLICIT_VALS, bool FILTER, bool WRITE_KEYS>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__ keys_in,
-                                                           const uint32_t *__restrict__ vals_in,
-                                                           K *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
-                                                           const uint32_t *n_ptr, uint32_t n_fixed, int shift,
-                                                           const uint32_t *__restrict__ digit_count,
-                                                           uint32_t *lookback, uint32_t *ticket) {
+__global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restrict__ keys_in,
+                                                              const uint32_t *__restrict__ vals_in,
+                                                              K *__restrict__ keys_out,
+                                                              uint32_t *__restrict__ vals_out, const uint32_t *n_ptr,
+                                                              uint32_t n_fixed, int shift,
+                                                              const uint32_t *__restrict__ digit_count,
+                                                              uint32_t *lookback, uint32_t *ticket) {
     __shared__ uint32_t s_whist[kWarps][256];
     __shared__ uint32_t s_digit_base[256];
     __shared__ uint32_t s_dig_out[256];
@@ -62,45 +63,40 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
         const size_t base = (size_t)bid * kSortTile;
         if (base >= n) break;
 
-        K key[kSortItems];
-        uint32_t val[kSortItems];
-        uint32_t rank[kSortItems];
-        uint32_t dig[kSortItems];
-        bool valid[kSortItems];
-        const size_t wbase = base + (size_t)warp * 32 * kSortItems;
+        // 1. keys (values are re-read at scatter time to keep registers low: 4 CTAs / SM)
+        uint32_t key[kSortItems];
+        uint32_t rank2[kSortItems / 2];  // two 16-bit in-warp ranks per register
+        const size_t wbase = base + (size_t)warp * 32 * kSortItems + lane;
 #pragma unroll
         for (int j = 0; j < kSortItems; ++j) {
-            const size_t idx = wbase + (size_t)j * 32 + lane;
-            valid[j] = idx < n;
-            key[j] = 0;
-            val[j] = 0;
-            if (valid[j]) {
-                key[j] = keys_in[idx];
-                val[j] = IMPLICIT_VALS ? (uint32_t)idx : vals_in[idx];
-                if (FILTER && key[j] == (K)kNoTiles) valid[j] = false;
-            }
-            dig[j] = digit_of(key[j], shift);
+            const size_t idx = wbase + (size_t)j * 32;
+            key[j] = idx < n ? (uint32_t)keys_in[idx] : 0xFFFFFFFFu;
         }
-        // warp-level stable ranking
+        // 2. warp-level stable ranking (8 ballots per item = match on the digit)
 #pragma unroll
         for (int j = 0; j < kSortItems; ++j) {
-            uint32_t peers = __ballot_sync(0xffffffffu, valid[j]);
+            const size_t idx = wbase + (size_t)j * 32;
+            const bool valid = idx < n && (!FILTER || key[j] != kNoTiles);
+            const uint32_t d = digit_of(key[j], shift);
+            uint32_t peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
             for (int b = 0; b < 8; ++b) {
-                const bool bit = (dig[j] >> b) & 1u;
+                const bool bit = (d >> b) & 1u;
                 const uint32_t bal = __ballot_sync(0xffffffffu, bit);
                 peers &= bit ? bal : ~bal;
             }
             const uint32_t lt = __popc(peers & lanemask_lt);
             uint32_t prev = 0;
-            if (valid[j]) prev = s_whist[warp][dig[j]];
+            if (valid) prev = s_whist[warp][d];
             __syncwarp();
-            if (valid[j] && lt == 0) s_whist[warp][dig[j]] = prev + __popc(peers);
+            if (valid && lt == 0) s_whist[warp][d] = prev + __popc(peers);
             __syncwarp();
-            rank[j] = prev + lt;
+            const uint32_t r = valid ? prev + lt : 0xFFFFu;
+            if (j & 1) rank2[j >> 1] |= r << 16;
+            else rank2[j >> 1] = r;
         }
         __syncthreads();
-        // thread tid owns digit tid: exclusive scan across warps, tile total
+        // 3. thread tid owns digit tid: exclusive scan across warps, tile total, look-back
         uint32_t tot = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
@@ -108,7 +104,6 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
             s_whist[w][tid] = tot;
             tot += c;
         }
-        // decoupled look-back for digit tid
         {
             volatile uint32_t *lb = lookback + (size_t)bid * 256 + tid;
             uint32_t prefix = 0;
@@ -116,13 +111,36 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
                 *lb = kFlagInc | tot;
             } else {
                 *lb = kFlagAgg | tot;
-                const volatile uint32_t *pp = lookback + (size_t)(bid - 1) * 256 + tid;
+                // walk back kLB predecessors per round trip (independent loads in flight)
+                constexpr int kLB = 8;
+                int p = (int)bid - 1;
                 for (;;) {
-                    uint32_t v;
-                    do { v = *pp; } while ((v & ~kValMask) == 0);
-                    prefix += v & kValMask;
-                    if ((v & ~kValMask) == kFlagInc) break;
-                    pp -= 256;
+                    uint32_t v[kLB];
+#pragma unroll
+                    for (int q = 0; q < kLB; ++q)
+                        v[q] = p - q >= 0 ? ((const volatile uint32_t *)lookback)[(size_t)(p - q) * 256 + tid]
+                                          : kFlagInc;  // before CTA 0: a virtual inclusive 0
+                    int used = kLB;
+                    bool inc = false;
+                    uint32_t add = 0;
+#pragma unroll
+                    for (int q = 0; q < kLB; ++q) {
+                        if (used == kLB) {
+                            const uint32_t f = v[q] & ~kValMask;
+                            if (f == 0) {
+                                used = q;  // not yet published: re-read from here
+                            } else {
+                                add += v[q] & kValMask;
+                                if (f == kFlagInc) {
+                                    inc = true;
+                                    used = q + 1;
+                                }
+                            }
+                        }
+                    }
+                    prefix += add;
+                    p -= used;
+                    if (inc) break;
                 }
                 *lb = kFlagInc | (prefix + tot);
             }
@@ -131,15 +149,20 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const K *__restrict__
         uint32_t tile_total;
         s_blk_start[tid] = block_exclusive_scan_256(tot, s_scan, tile_total);
         __syncthreads();
+        // 4. scatter into shared memory in tile-sorted order (values loaded now, coalesced)
 #pragma unroll
         for (int j = 0; j < kSortItems; ++j) {
-            if (valid[j]) {
-                const uint32_t pos = s_blk_start[dig[j]] + s_whist[warp][dig[j]] + rank[j];
-                s_keys[pos] = key[j];
-                s_vals[pos] = val[j];
+            const uint32_t r = (rank2[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
+            if (r != 0xFFFFu) {
+                const size_t idx = wbase + (size_t)j * 32;
+                const uint32_t d = digit_of(key[j], shift);
+                const uint32_t pos = s_blk_start[d] + s_whist[warp][d] + r;
+                s_keys[pos] = (K)key[j];
+                s_vals[pos] = IMPLICIT_VALS ? (uint32_t)idx : __ldg(vals_in + idx);
             }
         }
         __syncthreads();
+        // 5. write out contiguous digit runs
         for (uint32_t i = tid; i < tile_total; i += kSortThreads) {
             const K k = s_keys[i];
             const uint32_t d = digit_of(k, shift);
@@ -203,12 +226,12 @@ __global__ void __launch_bounds__(1024) k_tile_finalize(const uint32_t *__restri
 
 // The paper's sorted key array, materialised for inspection: keys[j] = tile << 32 | depth.
 __global__ void k_sorted_keys(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ sorted_value,
-                              const float4 *__restrict__ rec, uint64_t *__restrict__ keys) {
+                              const uint32_t *__restrict__ depth_key, uint64_t *__restrict__ keys) {
     const int tile = blockIdx.x;
     const uint2 r = ranges[tile];
     for (uint32_t j = r.x + threadIdx.x; j < r.y; j += blockDim.x) {
         const uint32_t g = sorted_value[j];
-        keys[j] = ((uint64_t)tile << 32) | __float_as_uint(rec[3 * (size_t)g + 1].w);
+        keys[j] = ((uint64_t)tile << 32) | depth_key[g];
     }
 }
 
@@ -275,7 +298,7 @@ cudaError_t launch_sorted_keys(void *ws, const Layout &L, uint64_t *keys, cudaSt
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
     k_sorted_keys<<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
-                                              at<const float4>(ws, P.rec), keys);
+                                              at<const uint32_t>(ws, P.depth_key), keys);
     return cudaGetLastError();
 }
 

@@ -91,13 +91,21 @@ class Rasterizer:
 
     # views of the intermediates (zero-copy)
     def records(self) -> torch.Tensor:
+        """[N, 12] float32 render records: (x, y, a, b | c, t, sigma, hx | hy, r, g, b); valid
+        only where depth_keys() != 0xFFFFFFFF."""
         return self._view(self.layout.rec, 12 * self.scene.n, torch.float32).view(self.scene.n, 12)
 
-    def bininfo(self) -> torch.Tensor:
-        return self._view(self.layout.bininfo, 4 * self.scene.n, torch.int32).view(self.scene.n, 4)
+    def emit_records(self) -> torch.Tensor:
+        """[N, 8] int32 emission records: (count, info, span0..3, aux0, aux1)."""
+        return self._view(self.layout.erec, 8 * self.scene.n, torch.int32).view(self.scene.n, 8)
 
     def counts(self) -> torch.Tensor:
-        return self.bininfo()[:, 2]
+        """Per-Gaussian tile count of the current frame (int32, 0 for Gaussians without tiles)."""
+        c = self.emit_records()[:, 0]
+        return torch.where(self.depth_keys() == -1, torch.zeros_like(c), c)
+
+    def depth_keys(self) -> torch.Tensor:
+        return self._view(self.layout.depth_key, self.scene.n, torch.int32)
 
     def order(self) -> torch.Tensor:
         return self._view(self.layout.order, self.scene.n, torch.int32)
@@ -161,11 +169,11 @@ class Rasterizer:
 
     def render_stats(self, stream=None) -> dict:
         """Work counts of the render for the current frame (measurement; synchronises)."""
-        c = torch.zeros(4, dtype=torch.int64, device=self.device)
+        c = torch.zeros(5, dtype=torch.int64, device=self.device)
         check(lib().ss_render_stats(C.byref(self.frame), C.c_void_p(c.data_ptr()),
                                     C.c_void_p(_stream_handle(stream))), "ss_render_stats")
         v = c.cpu().tolist()
-        return {"E_pix": v[0], "E_blend": v[1], "E_cta": v[2], "pixels": v[3]}
+        return {"E_pix": v[0], "E_blend": v[1], "E_cta": v[2], "pixels": v[3], "E_kept": v[4]}
 
     def prune_score(self, score: torch.Tensor, bg=(0.0, 0.0, 0.0), stream=None) -> torch.Tensor:
         assert score.dtype == torch.float64 and score.numel() == self.scene.n and score.is_cuda

@@ -31,7 +31,7 @@ def test_layout_and_workspace(lib):
     L = _abi.layout(1000, 4096, 256, 256)
     assert (L.tiles_x, L.tiles_y, L.n_tiles, L.tile_bits) == (16, 16, 256, 8)
     assert L.total_bytes == _abi.workspace_size(1000, 4096, 256, 256)
-    offs = sorted([L.rec, L.bininfo, L.depth_key, L.order, L.pair_tile, L.pair_value, L.sorted_value,
+    offs = sorted([L.rec, L.erec, L.depth_key, L.order, L.pair_tile, L.pair_value, L.sorted_value,
                    L.ranges, L.tile_count, L.n_visible, L.total_pairs, L.overflow])
     assert len(set(offs)) == len(offs) and all(o % 256 == 0 for o in offs)
     L2 = _abi.layout(10, 100, 1297, 840)

@@ -33,7 +33,9 @@ def _gpu_frame(scene, cam, mode, bg=(0.0, 0.0, 0.0), capacity=None):
     P = tot["pairs"]
     out = dict(
         rz=rz, img=img.cpu().numpy(), T=T.cpu().numpy(), nc=nc.cpu().numpy().astype(np.uint32),
-        rec=rz.records().cpu().numpy(), bininfo=rz.bininfo().cpu().numpy().view(np.uint32),
+        rec=rz.records().cpu().numpy(), counts=rz.counts().cpu().numpy().view(np.uint32),
+        erec=rz.emit_records().cpu().numpy().view(np.uint32),
+        depth_key=rz.depth_keys().cpu().numpy().view(np.uint32),
         order=rz.order().cpu().numpy().view(np.uint32)[:tot["n_visible"]],
         values=rz.sorted_values().cpu().numpy().view(np.uint32)[:P],
         keys=rz.sorted_keys().cpu().numpy().view(np.uint64)[:P],
@@ -46,18 +48,26 @@ def _check_frame(scene, cam, mode, bg=(0.0, 0.0, 0.0), capacity=None, image=True
     g = _gpu_frame(scene, cam, mode, bg, capacity)
     f = oracle.frame(scene, cam, mode, bg, render=image)
     assert g["overflow"] == 0
-    cnt = g["bininfo"][:, 2]
+    cnt = g["counts"]
     assert np.array_equal(cnt, f.counts), "tile counts differ"
     vis = cnt > 0
-    # records (bit-exact): GPU (x,y,a,b | c,t,sigma,depth | r,g,b,0); oracle (x,y,depth,a,b,c,sigma,t,r,g,b,vis)
+    # records (bit-exact): GPU (x,y,a,b | c,t,sigma,hx | hy,r,g,b); oracle (x,y,depth,a,b,c,sigma,t,r,g,b,vis)
     gr, orr = g["rec"][vis], f.rec[vis]
-    pairs = [(0, 0), (1, 1), (2, 3), (3, 4), (4, 5), (5, 7), (6, 6), (7, 2), (8, 8), (9, 9), (10, 10)]
+    pairs = [(0, 0), (1, 1), (2, 3), (3, 4), (4, 5), (5, 7), (6, 6), (9, 8), (10, 9), (11, 10)]
     for gi, oi in pairs:
         assert np.array_equal(gr[:, gi].view(np.uint32), orr[:, oi].view(np.uint32)), f"record field {gi}"
-    # rect (3-sigma / SnugBox rect; AccuTile: SnugBox rect)
-    gb = g["bininfo"][vis]
-    rect = np.stack([gb[:, 0] & 0xFFFF, gb[:, 0] >> 16, gb[:, 1] & 0xFFFF, gb[:, 1] >> 16], 1)
-    assert np.array_equal(rect.astype(np.int32), f.rect[vis])
+    assert np.array_equal(g["depth_key"][vis], orr[:, 2].view(np.uint32)), "depth keys"
+    assert np.all(g["depth_key"][~vis] == 0xFFFFFFFF)
+    er = g["erec"][vis]
+    if mode == "accutile":  # aux = t as float64 bits: 2 log(255 sigma) of the stored sigma
+        t64 = er[:, 6:8].copy().view(np.float64)[:, 0]
+        t_or = np.array([oracle.threshold(s) for s in orr[:, 6]])
+        assert np.all(np.abs(t64 - t_or) <= 4.5e-16 * np.abs(t_or))  # CUDA log vs glibc log (R2)
+    else:  # the packed tile rect
+        pr = er[:, 6]
+        x0, y0 = pr & 0xFF, (pr >> 16) & 0xFF
+        rect = np.stack([x0, x0 + ((pr >> 8) & 0xFF) + 1, y0, y0 + (pr >> 24) + 1], 1)
+        assert np.array_equal(rect.astype(np.int32), f.rect[vis])
     # depth order of the visible Gaussians: (depth bits, index) -- numpy's lexsort on the oracle records
     idx = np.nonzero(vis)[0]
     dbits = f.rec[idx, 2].view(np.uint32)
