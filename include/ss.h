@@ -101,9 +101,8 @@ typedef struct {
 
 /* Byte offsets of every sub-buffer inside the workspace (for inspection and tests).
  * Records of a Gaussian with >= 1 tile (written only for those):
- *   rec  (48 B, render): q0 = (x2d, y2d, a, b), q1 = (c, t, sigma, hx), q2 = (hy, r, g, b)
- *        (a, b, c) = conic Sigma_2D^-1 (Eq. 10); t = 2 log(255 sigma) (Eq. 11); (hx, hy) =
- *        SnugBox half-extents widened by the float32 error bound of the render's q
+ *   rec  (48 B, render): q0 = (x2d, y2d, a, b), q1 = (c, t, sigma, 0), q2 = (0, r, g, b)
+ *        (a, b, c) = conic Sigma_2D^-1 (Eq. 10); t = 2 log(255 sigma) (Eq. 11)
  *   erec (32 B, emission, one aligned sector): e0 = (count, info, span0, span1),
  *        e1 = (span2, span3, aux0, aux1); info = nspans | inline << 8 | columns << 9; a span
  *        is first tile (16 b) | length << 16 | column-step << 31; aux = t as float64 bits
@@ -183,6 +182,22 @@ SS_API ss_status ss_render_stats(const ss_frame *frame /*host*/, uint64_t *count
  * Requires ss_sort on the frame. */
 SS_API ss_status ss_prune_score(const ss_frame *frame /*host*/, const float *bg /*host [3]*/, double *score,
                          void *stream);
+
+/* Prune step (Sec. 4.2 P:381 "removing a set percentage with the lowest
+ * sensitivities", Soft Pruning P:422-425, Hard Pruning P:434-436).
+ * ss_prune_select: keep[i] (device uint8 [n]) = 0 for exactly k = ss_prune_count(n, ratio) =
+ * floor(ratio n) Gaussians with the smallest score (device float64 [n], e.g. the all-reduced
+ * U~); on equal scores the higher index is removed first.  ratio in [0, 1].
+ * ss_compact_scene: stable stream compaction of every SoA plane of `in` into `out` (device
+ * planes allocated by the caller for out->n = n - k Gaussians; out->sh planes have stride
+ * out->n); *n_out (device uint32) receives the survivor count.  Both use a caller workspace
+ * of ss_prune_workspace_size(n) bytes (device). */
+SS_API size_t ss_prune_workspace_size(int32_t n);
+SS_API uint32_t ss_prune_count(int32_t n, double ratio);
+SS_API ss_status ss_prune_select(const double *score, int32_t n, double ratio, uint8_t *keep, void *ws,
+                                 size_t ws_bytes, void *stream);
+SS_API ss_status ss_compact_scene(const ss_scene *in /*host*/, const uint8_t *keep, const ss_scene *out /*host*/,
+                                  uint32_t *n_out, void *ws, size_t ws_bytes, void *stream);
 
 /* Convenience: ss_preprocess + ss_bin + ss_sort + ss_render in one call. */
 SS_API ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,

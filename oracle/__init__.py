@@ -67,6 +67,7 @@ def lib():
             "or_composite_alphas": (None, [i, vp, vp, vp, vp]),
             "or_render_tiles": (None, [vp, vp, vp, i, i, vp, vp, i, vp, vp, vp]),
             "or_prune_score_tiles": (None, [vp, vp, vp, i, i, vp, vp, vp, i]),
+            "or_prune_select": (C.c_int64, [i, vp, d, vp]),
             "or_frame": (u64, [i, i, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp, vp, vp, u64, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
@@ -289,3 +290,11 @@ def prune_score_tiles(rec, values, ranges, width, height, tiles, bg=(0.0, 0.0, 0
                                _p(np.ascontiguousarray(ranges, np.uint32)), width, height,
                                _p(np.asarray(bg, np.float32)), _p(score), _p(tl), len(tl))
     return score
+
+
+def prune_select(score: np.ndarray, ratio: float):
+    """keep mask (uint8) and k = floor(ratio * N) removed (lowest scores, higher index first on ties)."""
+    score = np.ascontiguousarray(score, np.float64)
+    keep = np.zeros(len(score), np.uint8)
+    k = lib().or_prune_select(len(score), _p(score), float(ratio), _p(keep))
+    return keep, int(k)

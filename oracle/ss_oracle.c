@@ -754,3 +754,35 @@ void or_prune_score_tiles(const float *rec, const uint32_t *values, const uint32
         or_prune_score(rec, values, ranges, width, bg, score, tx * TILE, x1, ty * TILE, y1);
     }
 }
+
+/* ------------------------------------------------------------------------------------
+ * Prune selection (Sec. 4.2: "removing a set percentage with the lowest sensitivities",
+ * P:381; Soft Pruning P:422-425, Hard Pruning P:434-436): remove exactly
+ * k = floor(ratio * N) Gaussians with the smallest score U~; among equal scores the higher
+ * canonical index is removed first (the lower index is kept).  keep[i] = 1 for survivors.
+ * Plain definition: order all indices by (score ascending, index descending), remove the
+ * first k.  Returns k.
+ * ---------------------------------------------------------------------------------- */
+static const double *g_sel_score;
+static int cmp_prune(const void *pa, const void *pb)
+{
+    int a = *(const int *)pa, b = *(const int *)pb;
+    double sa = g_sel_score[a], sb = g_sel_score[b];
+    if (sa < sb) return -1;
+    if (sa > sb) return 1;
+    return (a > b) ? -1 : (a < b ? 1 : 0); /* equal scores: higher index first */
+}
+
+int64_t or_prune_select(int n, const double *score, double ratio, uint8_t *keep)
+{
+    int64_t k = (int64_t)floor(ratio * (double)n);
+    if (k < 0) k = 0;
+    if (k > n) k = n;
+    int *idx = (int *)malloc(sizeof(int) * (size_t)(n > 0 ? n : 1));
+    for (int i = 0; i < n; ++i) { idx[i] = i; keep[i] = 1; }
+    g_sel_score = score;
+    qsort(idx, (size_t)n, sizeof(int), cmp_prune);
+    for (int64_t j = 0; j < k; ++j) keep[idx[j]] = 0;
+    free(idx);
+    return k;
+}

@@ -25,6 +25,7 @@ UNITS = {
     "ss_geometry.cu": ["--fmad=false"],
     "ss_sort.cu": [],
     "ss_render.cu": [],
+    "ss_prune.cu": [],
 }
 HEADERS = ["ss_common.cuh"]
 

@@ -1,6 +1,7 @@
 // ss_api.cu -- the extern "C" boundary of libss.so (declared in include/ss.h).
 // Host-side validation, workspace layout and the launch sequence of each call.
 #include <cstdio>
+#include <cmath>
 #include <cstring>
 
 #include "ss_common.cuh"
@@ -206,6 +207,35 @@ ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mo
     if (s == SS_OK) s = ss_sort(frame, stream);
     if (s == SS_OK) s = ss_render(frame, bg, out_rgb, out_T, out_ncontrib, stream);
     return s;
+}
+
+size_t ss_prune_workspace_size(int32_t n) { return n < 0 ? 0 : prune_workspace_bytes(n); }
+
+uint32_t ss_prune_count(int32_t n, double ratio) {
+    if (n <= 0) return 0;
+    double kd = floor(ratio * (double)n);
+    if (kd < 0.0) kd = 0.0;
+    if (kd > (double)n) kd = (double)n;
+    return (uint32_t)kd;
+}
+
+ss_status ss_prune_select(const double *score, int32_t n, double ratio, uint8_t *keep, void *ws, size_t ws_bytes,
+                          void *stream) {
+    if (n < 0 || !(ratio >= 0.0) || !(ratio <= 1.0)) return SS_ERR_INVALID_ARG;
+    if (n >= (1 << 30)) return SS_ERR_UNSUPPORTED;
+    if (n > 0 && (!score || !keep)) return SS_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < prune_workspace_bytes(n)) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_prune_select(score, n, ratio, keep, ws, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_compact_scene(const ss_scene *in, const uint8_t *keep, const ss_scene *out, uint32_t *n_out,
+                           void *ws, size_t ws_bytes, void *stream) {
+    if (!in || !out || !n_out || in->n < 0 || in->sh_degree < 0 || in->sh_degree > 3) return SS_ERR_INVALID_ARG;
+    if (out->sh_degree != in->sh_degree || out->n < 0 || out->n > in->n) return SS_ERR_INVALID_ARG;
+    if (in->n > 0 && (!keep || !in->mean_opac || !in->scale || !in->rot || !in->sh)) return SS_ERR_INVALID_ARG;
+    if (out->n > 0 && (!out->mean_opac || !out->scale || !out->rot || !out->sh)) return SS_ERR_INVALID_ARG;
+    if (!ws || ws_bytes < prune_workspace_bytes(in->n)) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_compact(*in, keep, *out, (uint32_t)out->n, n_out, ws, static_cast<cudaStream_t>(stream)));
 }
 
 const char *ss_status_string(ss_status s) {

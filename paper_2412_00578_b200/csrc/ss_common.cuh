@@ -74,6 +74,12 @@ cudaError_t launch_render_stats(void *ws, const Layout &L, int W, int H, unsigne
 cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2,
                                double *score, cudaStream_t st);
 
+size_t prune_workspace_bytes(int32_t n);
+cudaError_t launch_prune_select(const double *score, int32_t n, double ratio, uint8_t *keep, void *ws,
+                                cudaStream_t st);
+cudaError_t launch_compact(const ss_scene &in, const uint8_t *keep, const ss_scene &out, uint32_t out_stride,
+                           uint32_t *n_out, void *ws, cudaStream_t st);
+
 // Exclusive scan of one value per thread over a 256-thread CTA (8 warps); `total` gets the
 // CTA sum.  Contains two __syncthreads: every thread of the CTA must call it.
 __device__ __forceinline__ uint32_t block_exclusive_scan_256(uint32_t v, uint32_t *s_warp, uint32_t &total) {

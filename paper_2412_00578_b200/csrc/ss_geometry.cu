@@ -226,6 +226,8 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         uint32_t count = 0;
         const float4 mo = mean_opac[i];
+        const float4 q4 = rot[i];    // issued with the mean: one memory round trip, not two
+        const float4 s4 = scale[i];
         const float px = cam.V[0] * mo.x + cam.V[1] * mo.y + cam.V[2] * mo.z + cam.V[3];
         const float py = cam.V[4] * mo.x + cam.V[5] * mo.y + cam.V[6] * mo.z + cam.V[7];
         const float pz = cam.V[8] * mo.x + cam.V[9] * mo.y + cam.V[10] * mo.z + cam.V[11];
@@ -240,12 +242,6 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             const float tx = px / pz, ty = py / pz;
             x2d = cam.fx * tx + cam.cx;
             y2d = cam.fy * ty + cam.cy;
-            // likely visible: start pulling its SH planes into L2 now, so the colour loads
-            // after the (float64) tile count hit L2 instead of HBM
-            if (x2d > -0.25f * cam.W && x2d < 1.25f * cam.W && y2d > -0.25f * cam.H && y2d < 1.25f * cam.H) {
-#pragma unroll
-                for (int p = 0; p < NP; ++p) asm volatile("prefetch.global.L2 [%0];" ::"l"(sh + (size_t)p * n + i));
-            }
             float txc = tx, tyc = ty;
             if (cam.clip > 0.0f) {
                 const float limx = cam.clip * ((0.5f * (float)cam.W) / cam.fx);
@@ -255,8 +251,6 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             }
             const float j00 = cam.fx / pz, j02 = -(cam.fx * txc) / pz;
             const float j11 = cam.fy / pz, j12 = -(cam.fy * tyc) / pz;
-            const float4 q4 = rot[i];
-            const float4 s4 = scale[i];
             const float qn = 1.0f / sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
             const float w = q4.x * qn, x = q4.y * qn, y = q4.z * qn, z = q4.w * qn;
             const float Rm[3][3] = {
@@ -353,21 +347,11 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             rgb0 = acc0 > 0.0f ? acc0 : 0.0f;
             rgb1 = acc1 > 0.0f ? acc1 : 0.0f;
             rgb2 = acc2 > 0.0f ? acc2 : 0.0f;
-            // render-side culling box: SnugBox half-extents widened by the float32 error bound
-            // of the render's q (|dq| <= 16 eps cond(conic) q, cond <= (a+c)^2/D) + 1e-3 px
-            float hxr = 1e-3f, hyr = 1e-3f;
-            if (td > 0.0) {
-                const double ad = a, cd = c;
-                const double D = ad * cd - (double)b * (double)b;
-                const double widen = 1.0 + 16.0 * 5.9604644775390625e-08 * ((ad + cd) * (ad + cd) / D);
-                hxr = __double2float_ru(snug.hx * widen + 1e-3);
-                hyr = __double2float_ru(snug.hy * widen + 1e-3);
-            }
-            // render record (48 B): q0 (x, y, a, b) | q1 (c, t, sigma, hx) | q2 (hy, r, g, b)
+            // render record (48 B): q0 (x, y, a, b) | q1 (c, t, sigma, 0) | q2 (0, r, g, b)
             float4 *q = rec + 3 * (size_t)i;
             q[0] = make_float4(x2d, y2d, a, b);
-            q[1] = make_float4(c, (float)td, mo.w, hxr);
-            q[2] = make_float4(hyr, rgb0, rgb1, rgb2);
+            q[1] = make_float4(c, (float)td, mo.w, 0.0f);
+            q[2] = make_float4(0.0f, rgb0, rgb1, rgb2);
             // emission record (32 B, one sector): e0 (count, info, span0, span1), e1 (span2, span3,
             // aux0, aux1); info = nspans | inline flag << 8 | columns flag << 9; aux = t as float64
             // bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1) for the fallback path.
@@ -489,7 +473,7 @@ __global__ void __launch_bounds__(kEmitBlock, 3) k_emit(int mode, const float4 *
     __shared__ uint32_t s_gid[kSpanCap];
     __shared__ uint32_t s_pfx[kSpanCap];   // exclusive prefix of span lengths within the round
     __shared__ uint32_t s_warp[8];
-    __shared__ uint32_t s_bid, s_base, s_total, s_nspans;
+    __shared__ uint32_t s_bid, s_base, s_nspans;
     const bool lb_warp = threadIdx.x >= kEmitThreads;
     const int lane = threadIdx.x & 31;
     for (int t = threadIdx.x; t < (smem_hist ? n_tiles : 0); t += blockDim.x) s_tile_hist[t] = 0;

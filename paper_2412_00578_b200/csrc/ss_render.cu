@@ -19,7 +19,7 @@ constexpr int kBatch = 256;
 // Shared-memory batch of gathered records, split by use: the per-warp culling box, the conic
 // (skip test), the colour.
 struct Batch {
-    float4 box[kBatch];  // x, y, hx, hy  (hx, hy: conservative alpha >= 1/255 half-extents)
+    float4 box[kBatch];  // x, y, -, -
     float4 con[kBatch];  // a, 2b, c, t
     float4 col[kBatch];  // r, g, b, sigma
 };
@@ -46,7 +46,7 @@ __device__ __forceinline__ void load_batch(Batch &s, const uint32_t *__restrict_
         const float4 q0 = __ldg(rec + 3 * (size_t)g + 0);  // x, y, a, b
         const float4 q1 = __ldg(rec + 3 * (size_t)g + 1);  // c, t, sigma, hx
         const float4 q2 = __ldg(rec + 3 * (size_t)g + 2);  // hy, r, g, b
-        s.box[threadIdx.x] = make_float4(q0.x, q0.y, q1.w, q2.x);
+        s.box[threadIdx.x] = make_float4(q0.x, q0.y, 0.0f, 0.0f);
         s.con[threadIdx.x] = make_float4(q0.z, q0.w + q0.w, q1.x, q1.y);
         s.col[threadIdx.x] = make_float4(q2.y, q2.z, q2.w, q1.z);
         if (s_id) s_id[threadIdx.x] = g;

@@ -45,6 +45,8 @@ class DeviceScene:
 
 
 def camera_struct(cam) -> SsCamera:
+    if isinstance(cam, SsCamera):
+        return cam
     c = SsCamera()
     c.viewmat[:] = [float(v) for v in np.asarray(cam.viewmat, np.float32).reshape(-1)]
     c.fx, c.fy, c.cx, c.cy = float(cam.fx), float(cam.fy), float(cam.cx), float(cam.cy)
@@ -91,7 +93,7 @@ class Rasterizer:
 
     # views of the intermediates (zero-copy)
     def records(self) -> torch.Tensor:
-        """[N, 12] float32 render records: (x, y, a, b | c, t, sigma, hx | hy, r, g, b); valid
+        """[N, 12] float32 render records: (x, y, a, b | c, t, sigma, 0 | 0, r, g, b); valid
         only where depth_keys() != 0xFFFFFFFF."""
         return self._view(self.layout.rec, 12 * self.scene.n, torch.float32).view(self.scene.n, 12)
 
@@ -232,3 +234,29 @@ def render_views_to_host(rz: Rasterizer, cams, host_out: list, bg=(0.0, 0.0, 0.0
             host_out[j].copy_(st["dev"][b], non_blocking=True)
             st["done"][b].record(st["copy"])
     st["copy"].synchronize()
+
+
+def prune(scene: DeviceScene, score: torch.Tensor, ratio: float, stream=None) -> tuple[DeviceScene, torch.Tensor]:
+    """The prune step (Sec. 4.2): drop floor(ratio * N) Gaussians with the smallest score (ties:
+    higher index first) and return the compacted scene plus the keep mask.  Every rank that
+    holds the same all-reduced score gets the same scene (no further exchange)."""
+    assert score.dtype == torch.float64 and score.numel() == scene.n and score.is_cuda
+    n = scene.n
+    k = int(lib().ss_prune_count(n, float(ratio)))
+    dev = scene.mean_opac.device
+    ws = torch.empty(int(lib().ss_prune_workspace_size(n)), dtype=torch.uint8, device=dev)
+    keep = torch.empty(n, dtype=torch.uint8, device=dev)
+    sh_handle = C.c_void_p(_stream_handle(stream))
+    check(lib().ss_prune_select(C.c_void_p(score.data_ptr()), n, float(ratio), C.c_void_p(keep.data_ptr()),
+                                C.c_void_p(ws.data_ptr()), ws.numel(), sh_handle), "ss_prune_select")
+    m = n - k
+    out = DeviceScene(torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
+                      torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
+                      torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
+                      torch.empty((scene.sh.shape[0], m, 4), dtype=torch.float32, device=dev), scene.sh_degree)
+    n_out = torch.zeros(1, dtype=torch.int32, device=dev)
+    src, dst = scene.struct(), out.struct()
+    check(lib().ss_compact_scene(C.byref(src), C.c_void_p(keep.data_ptr()), C.byref(dst),
+                                 C.c_void_p(n_out.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(), sh_handle),
+          "ss_compact_scene")
+    return out, keep

@@ -160,3 +160,25 @@ def test_score_additive_over_views_and_nonnegative():
     sab = oracle.score_views(scene, cams)
     assert np.allclose(sab, sa + sb, rtol=1e-12, atol=0)
     assert np.all(sab >= 0) and sab.max() > 0
+
+
+def test_prune_select_examples_and_invariants():
+    """Prune step (P:381 'removing a set percentage with the lowest sensitivities'); printed
+    examples S:389-392 and the argsort invariance of P:416 (log is monotone)."""
+    keep, k = oracle.prune_select(np.arange(10, dtype=np.float64), 0.3)
+    assert k == 3 and keep.sum() == 7 and keep[:3].sum() == 0
+    keep, k = oracle.prune_select(np.ones(10), 0.5)          # ties: the last 5 by index go
+    assert keep.tolist() == [1] * 5 + [0] * 5
+    keep, k = oracle.prune_select(np.array([5.0, 1.0, 3.0, 0.0]), 0.5)
+    assert keep.tolist() == [1, 0, 1, 0]
+    rng = np.random.default_rng(7)
+    s = rng.integers(0, 50, 10000).astype(np.float64) * rng.uniform(0.5, 2.0)  # many ties
+    for ratio in (0.0, 0.1, 0.3, 0.8, 1.0):
+        keep, k = oracle.prune_select(s, ratio)
+        assert k == int(np.floor(ratio * len(s))) and keep.sum() == len(s) - k
+        order = np.lexsort((-np.arange(len(s)), s))            # library: (score asc, index desc)
+        want = np.ones(len(s), np.uint8)
+        want[order[:k]] = 0
+        assert np.array_equal(keep, want)
+        keep2, _ = oracle.prune_select(s * 37.5, ratio)      # positive scaling: same set
+        assert np.array_equal(keep, keep2)
