@@ -96,18 +96,21 @@ double or_threshold(float sigma) { return 2.0 * log(255.0 * (double)sigma); }
 void or_snugbox(double mx, double my, double a, double b, double c, double t,
                 double *bbox /* xmin,xmax,ymin,ymax */, double *tangent /* 8: Bl, Br, Bt, Bb */)
 {
+    /* contract (R1): one reciprocal each of D, a and c; quotients are products with them */
     double D = a * c - b * b;
-    double hx = sqrt(t * c / D);
-    double hy = sqrt(t * a / D);
+    double rD = 1.0 / D;
+    double hx = sqrt(t * c * rD);
+    double hy = sqrt(t * a * rD);
     bbox[0] = mx - hx;
     bbox[1] = mx + hx;
     bbox[2] = my - hy;
     bbox[3] = my + hy;
     if (tangent) {
-        tangent[0] = mx - hx; tangent[1] = my + b * hx / c;
-        tangent[2] = mx + hx; tangent[3] = my - b * hx / c;
-        tangent[4] = mx + b * hy / a; tangent[5] = my - hy;
-        tangent[6] = mx - b * hy / a; tangent[7] = my + hy;
+        double ia = 1.0 / a, ic = 1.0 / c;
+        tangent[0] = mx - hx; tangent[1] = my + b * hx * ic;
+        tangent[2] = mx + hx; tangent[3] = my - b * hx * ic;
+        tangent[4] = mx + b * hy * ia; tangent[5] = my - hy;
+        tangent[6] = mx - b * hy * ia; tangent[7] = my + hy;
     }
 }
 
@@ -182,13 +185,15 @@ static void intersect_line(double m_sweep_free, double m_line, double a_free, do
 {
     /* Eq. 15 with the roles named generically: on the line (coordinate `line` along the
      * swept axis), solve a_free u^2 + 2 b u v + c_line v^2 = t for u (free axis offset),
-     * v = line - m_line:  u = (-b v +- sqrt((b^2 - a_free c_line) v^2 + t a_free)) / a_free */
+     * v = line - m_line:  u = (-b v +- sqrt((b^2 - a_free c_line) v^2 + t a_free)) / a_free
+     * (contract R1: the quotient is a product with 1 / a_free) */
     double v = line - m_line;
     double disc = (b * b - a_free * c_line) * v * v + t * a_free;
     if (disc < 0.0) disc = 0.0; /* R12 */
     double s = sqrt(disc);
-    *lo = m_sweep_free + (-b * v - s) / a_free;
-    *hi = m_sweep_free + (-b * v + s) / a_free;
+    double ia = 1.0 / a_free;
+    *lo = m_sweep_free + (-b * v - s) * ia;
+    *hi = m_sweep_free + (-b * v + s) * ia;
 }
 
 uint32_t or_accutile(double mx, double my, double a, double b, double c, double t, int tiles_x,
@@ -342,8 +347,10 @@ void or_project(int n, int sh_degree, const float *mean_opac, const float *scale
         float py = V[4] * mx + V[5] * my + V[6] * mz + V[7];
         float pz = V[8] * mx + V[9] * my + V[10] * mz + V[11];
         if (!(pz >= cam->z_near)) continue;
-        /* perspective projection to pixel coordinates (R3) */
-        float tx = px / pz, ty = py / pz;
+        /* perspective projection to pixel coordinates (R3); contract R1: quotients by z are
+         * products with one reciprocal 1/z */
+        float iz = 1.0f / pz;
+        float tx = px * iz, ty = py * iz;
         float x2d = cam->fx * tx + cam->cx;
         float y2d = cam->fy * ty + cam->cy;
         /* Jacobian of the perspective projection at p_cam (R5: clamped tx/ty) */
@@ -354,8 +361,8 @@ void or_project(int n, int sh_degree, const float *mean_opac, const float *scale
             txc = fminf(limx, fmaxf(-limx, tx));
             tyc = fminf(limy, fmaxf(-limy, ty));
         }
-        float j00 = cam->fx / pz, j02 = -(cam->fx * txc) / pz;
-        float j11 = cam->fy / pz, j12 = -(cam->fy * tyc) / pz;
+        float j00 = cam->fx * iz, j02 = -(cam->fx * txc) * iz;
+        float j11 = cam->fy * iz, j12 = -(cam->fy * tyc) * iz;
         /* rotation from the normalised quaternion (w, x, y, z) */
         float qw = rot[4 * i + 0], qx = rot[4 * i + 1], qy = rot[4 * i + 2], qz = rot[4 * i + 3];
         float qn = 1.0f / sqrtf(qw * qw + qx * qx + qy * qy + qz * qz);
@@ -397,7 +404,8 @@ void or_project(int n, int sh_degree, const float *mean_opac, const float *scale
         /* colour (R13) */
         float dx = mx - cam->campos[0], dy = my - cam->campos[1], dz = mz - cam->campos[2];
         float len = sqrtf(dx * dx + dy * dy + dz * dz);
-        float ux = dx / len, uy = dy / len, uz = dz / len;
+        float il = 1.0f / len;
+        float ux = dx * il, uy = dy * il, uz = dz * il;
         float Y[16];
         or_sh_basis(sh_degree, ux, uy, uz, Y);
         float rgb[3];

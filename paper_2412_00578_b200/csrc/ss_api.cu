@@ -48,19 +48,24 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     L->pair_value2 = take(4 * Cap);
     P.sorted_value = take(4 * Cap);
     P.ranges = take(8 * T);
-    // ---- region cleared at the start of every frame
-    L->zero_begin = off;
-    P.tile_count = take(4 * T);
+    // ---- regions each call clears for itself (so every call is idempotent given its inputs)
+    L->zero_pre = off;  // written by ss_preprocess
     P.n_visible = take(4);
+    L->hist_depth = take(4 * 256 * kDepthPasses);
+    L->zero_pre_end = off;
+    L->zero_bin = off;  // written by ss_bin
+    P.tile_count = take(4 * T);
     P.total_pairs = take(4);
     P.overflow = take(4);
-    L->hist_depth = take(4 * 256 * kDepthPasses);
-    L->hist_tile = take(4 * 256 * 2);
     L->counters = take(4 * 16);
     L->lb_depth = take(4 * 256 * (size_t)L->nblk_depth * kDepthPasses);
-    L->lb_tile = take(4 * 256 * (size_t)L->nblk_tile * 2);
     L->lb_emit = take(4 * (size_t)L->nblk_emit);
-    L->zero_end = off;
+    L->zero_bin_end = off;
+    L->zero_sort = off;  // written by ss_sort
+    L->counters_sort = take(4 * 16);
+    L->lb_tile = take(4 * 256 * (size_t)L->nblk_tile * 2);
+    L->zero_sort_end = off;
+    L->hist_tile = take(4 * 256 * 2);
     P.total_bytes = off;
     return true;
 }
@@ -139,7 +144,7 @@ ss_status ss_preprocess(const ss_scene *scene, const ss_camera *cam, ss_bin_mode
     if (scene->n > 0 && (!scene->mean_opac || !scene->scale || !scene->rot || !scene->sh)) return SS_ERR_INVALID_ARG;
     if ((int)mode < 0 || (int)mode > 2) return SS_ERR_INVALID_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaMemsetAsync(at<char>(frame->ws, L.zero_begin), 0, L.zero_end - L.zero_begin, st);
+    cudaError_t e = cudaMemsetAsync(at<char>(frame->ws, L.zero_pre), 0, L.zero_pre_end - L.zero_pre, st);
     if (e != cudaSuccess) return cuda_status(e);
     return cuda_status(launch_preprocess(*scene, cam_args(*cam, L), (int)mode, frame->ws, L, st));
 }
@@ -151,7 +156,8 @@ ss_status ss_bin(const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame, 
     if ((s = check_cam(cam, frame)) != SS_OK) return s;
     if ((int)mode < 0 || (int)mode > 2) return SS_ERR_INVALID_ARG;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = launch_depth_sort(frame->ws, L, st);
+    cudaError_t e = cudaMemsetAsync(at<char>(frame->ws, L.zero_bin), 0, L.zero_bin_end - L.zero_bin, st);
+    if (e == cudaSuccess) e = launch_depth_sort(frame->ws, L, st);
     if (e == cudaSuccess) e = launch_emit(cam_args(*cam, L), (int)mode, frame->ws, L, st);
     return cuda_status(e);
 }
@@ -160,7 +166,10 @@ ss_status ss_sort(const ss_frame *frame, void *stream) {
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
-    return cuda_status(launch_tile_sort(frame->ws, L, static_cast<cudaStream_t>(stream)));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(at<char>(frame->ws, L.zero_sort), 0, L.zero_sort_end - L.zero_sort, st);
+    if (e == cudaSuccess) e = launch_tile_sort(frame->ws, L, st);
+    return cuda_status(e);
 }
 
 ss_status ss_sorted_keys(const ss_frame *frame, uint64_t *keys, void *stream) {

@@ -40,7 +40,10 @@ struct Layout {
     size_t dkA, dvA, dkB, dvB;      // depth sort ping-pong (uint32 [n])
     size_t pair_tile2;              // uint16 [capacity] tile-sort ping-pong
     size_t pair_value2;             // uint32 [capacity]
-    size_t zero_begin, zero_end;    // region cleared at the start of every frame
+    size_t zero_pre, zero_pre_end;    // regions each call clears for itself
+    size_t zero_bin, zero_bin_end;
+    size_t zero_sort, zero_sort_end;
+    size_t counters_sort;             // uint32 [16] tile-sort tickets / barrier / sort_n
     size_t hist_depth;              // uint32 [4][256]
     size_t hist_tile;               // uint32 [2][256]
     size_t counters;                // uint32 [16] block tickets

@@ -36,9 +36,12 @@ struct Snug {
 };
 
 __device__ __forceinline__ Snug snugbox(double mx, double my, double a, double b, double c, double t) {
+    // contract R1: one reciprocal each of D, a and c; quotients are products with them
     double D = a * c - b * b;
-    double hx = sqrt(t * c / D);
-    double hy = sqrt(t * a / D);
+    double rD = 1.0 / D;
+    double hx = sqrt(t * c * rD);
+    double hy = sqrt(t * a * rD);
+    double ia = 1.0 / a, ic = 1.0 / c;
     Snug s;
     s.hx = hx;
     s.hy = hy;
@@ -46,10 +49,10 @@ __device__ __forceinline__ Snug snugbox(double mx, double my, double a, double b
     s.xmax = mx + hx;
     s.ymin = my - hy;
     s.ymax = my + hy;
-    s.yl = my + b * hx / c;
-    s.yr = my - b * hx / c;
-    s.xt = mx + b * hy / a;
-    s.xb = mx - b * hy / a;
+    s.yl = my + b * hx * ic;
+    s.yr = my - b * hx * ic;
+    s.xt = mx + b * hy * ia;
+    s.xb = mx - b * hy * ia;
     return s;
 }
 
@@ -82,8 +85,9 @@ __device__ __forceinline__ void intersect_line(double m_free, double m_line, dou
     double disc = (b * b - a_free * c_line) * v * v + t * a_free;
     if (disc < 0.0) disc = 0.0;  // R12
     double s = sqrt(disc);
-    lo = m_free + (-b * v - s) / a_free;
-    hi = m_free + (-b * v + s) / a_free;
+    double ia = 1.0 / a_free;
+    lo = m_free + (-b * v - s) * ia;
+    hi = m_free + (-b * v + s) * ia;
 }
 
 // AccuTile, Algorithm 1 along the shorter side of the SnugBox tile rect (R9),
@@ -223,6 +227,9 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
     constexpr int NB = (DEG + 1) * (DEG + 1);
     constexpr int NP = (NB * 3 + 3) / 4;
     uint32_t my_vis = 0;
+    // camera constants of the J clamp (R5), the same values the per-Gaussian form would give
+    const float limx = cam.clip * ((0.5f * (float)cam.W) / cam.fx);
+    const float limy = cam.clip * ((0.5f * (float)cam.H) / cam.fy);
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         uint32_t count = 0;
         const float4 mo = mean_opac[i];
@@ -239,18 +246,17 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
         uint32_t spans[kInlineSpans] = {0u, 0u, 0u, 0u};
         uint32_t nspans = 0, cols = 0;
         if (pz >= cam.z_near) {
-            const float tx = px / pz, ty = py / pz;
+            const float iz = 1.0f / pz;  // contract R1: one reciprocal of z
+            const float tx = px * iz, ty = py * iz;
             x2d = cam.fx * tx + cam.cx;
             y2d = cam.fy * ty + cam.cy;
             float txc = tx, tyc = ty;
             if (cam.clip > 0.0f) {
-                const float limx = cam.clip * ((0.5f * (float)cam.W) / cam.fx);
-                const float limy = cam.clip * ((0.5f * (float)cam.H) / cam.fy);
                 txc = fminf(limx, fmaxf(-limx, tx));
                 tyc = fminf(limy, fmaxf(-limy, ty));
             }
-            const float j00 = cam.fx / pz, j02 = -(cam.fx * txc) / pz;
-            const float j11 = cam.fy / pz, j12 = -(cam.fy * tyc) / pz;
+            const float j00 = cam.fx * iz, j02 = -(cam.fx * txc) * iz;
+            const float j11 = cam.fy * iz, j12 = -(cam.fy * tyc) * iz;
             const float qn = 1.0f / sqrtf(q4.x * q4.x + q4.y * q4.y + q4.z * q4.z + q4.w * q4.w);
             const float w = q4.x * qn, x = q4.y * qn, y = q4.z * qn, z = q4.w * qn;
             const float Rm[3][3] = {
@@ -323,8 +329,9 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             // colour (R13): only Gaussians with tiles read their SH planes
             const float dx = mo.x - cam.cpx, dy = mo.y - cam.cpy, dz = mo.z - cam.cpz;
             const float len = sqrtf(dx * dx + dy * dy + dz * dz);
+            const float il = 1.0f / len;
             float Y[16];
-            sh_basis<DEG>(dx / len, dy / len, dz / len, Y);
+            sh_basis<DEG>(dx * il, dy * il, dz * il, Y);
             float hc[NP * 4];
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
@@ -656,7 +663,8 @@ cudaError_t launch_emit(const CamArgs &cam, int mode, void *ws, const Layout &L,
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int smem_hist = P.n_tiles <= 12288 ? 1 : 0;
     const size_t smem = smem_hist ? (size_t)P.n_tiles * 4 : 0;
-    cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (smem > 20 * 1024)  // static (~25 KB) + dynamic above the default 48 KB window
+        cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     const int grid = (int)L.nblk_emit < sms * 4 ? (int)L.nblk_emit : sms * 4;
     k_emit<<<grid, kEmitBlock, smem, st>>>(
         mode, at<const float4>(ws, P.rec), at<const uint4>(ws, P.erec), at<const uint32_t>(ws, P.order),

@@ -111,15 +111,19 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
             uint32_t last = st.last[pp];
             bool done = false;
             const int cnt = min((uint32_t)kBatch, range.y - start);
+            const uint32_t base = start - range.x + 1;
+            // branch-free blend: a non-contributing Gaussian gets alpha = 0, which leaves T and
+            // C bit-identical (T * 1 = T, fma(c, 0, C) = C), so only termination branches
+#pragma unroll 4
             for (int k = 0; k < cnt; ++k) {
                 const float4 bx = s.box[k];
                 const float4 cn = s.con[k];
-                const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
-                if (!(q <= cn.w)) continue;  // alpha < 1/255: no contribution (Eq. 9, R15)
                 const float4 cl = s.col[k];
-                const float alpha = alpha_of(q, cl.w);
+                const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
+                const bool contrib = q <= cn.w;  // alpha >= 1/255 (Eq. 9, R15)
+                const float alpha = contrib ? alpha_of(q, cl.w) : 0.0f;
                 const float Tn = T * (1.0f - alpha);
-                if (Tn < 1e-4f) {  // R16: stop before blending
+                if (Tn < 1e-4f) {  // R16: stop before blending (never for alpha = 0: T >= 1e-4)
                     done = true;
                     break;
                 }
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
                 C1 = fmaf(cl.y, w, C1);
                 C2 = fmaf(cl.z, w, C2);
                 T = Tn;
-                last = start - range.x + k + 1;
+                last = contrib ? base + (uint32_t)k : last;
             }
             st.T[pp] = T;
             st.C0[pp] = C0;
@@ -195,19 +199,21 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
             uint32_t last = st.last[pp];
             bool done = false;
             const int cnt = min((uint32_t)kBatch, range.y - start);
-            for (int k = 0; k < cnt; ++k) {
+            const uint32_t base = start - range.x + 1;
+#pragma unroll 4
+            for (int k = 0; k < cnt; ++k) {  // branch-free, as in k_render
                 const float4 bx = s.box[k];
                 const float4 cn = s.con[k];
                 const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
-                if (!(q <= cn.w)) continue;
-                const float alpha = alpha_of(q, s.col[k].w);
+                const bool contrib = q <= cn.w;
+                const float alpha = contrib ? alpha_of(q, s.col[k].w) : 0.0f;
                 const float Tn = T * (1.0f - alpha);
                 if (Tn < 1e-4f) {
                     done = true;
                     break;
                 }
                 T = Tn;
-                last = start - range.x + k + 1;
+                last = contrib ? base + (uint32_t)k : last;
             }
             st.T[pp] = T;
             st.last[pp] = last;
