@@ -52,5 +52,25 @@ def full(path):
                 print(f"  {key:75s} {r[i]:>14s} {units[i]}")
 
 
+def traffic(*paths):
+    """JSON {kernel: {"dram_bytes": read+write per launch (mean), "us": duration}} from full captures."""
+    import json
+    agg = collections.defaultdict(list)
+    for path in paths:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        hdr, units = rows[0], rows[1]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        ir, iw, it = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum"), \
+            hdr.index("gpu__time_duration.sum")
+        for r in rows[2:]:
+            name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("unnamed>::", "")
+            b = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
+            us = float(r[it]) * (1e-3 if units[it] == "nsecond" else 1.0)
+            agg[name].append((b, us))
+    print(json.dumps({k: {"dram_bytes": sum(b for b, _ in v) / len(v), "us": sum(u for _, u in v) / len(v),
+                          "captures": len(v)} for k, v in agg.items()}, indent=1))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](*sys.argv[2:])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
