@@ -166,10 +166,11 @@ def stage_bytes(stage, N, n_vis, P, n_tiles, W, H, sh_floats):
     """Algorithmic bytes per launch: what the step must move at minimum."""
     if stage == "preprocess":
         return 16 * N + (32 + 4 * sh_floats) * n_vis + 48 * n_vis + 4 * N
-    if stage == "bin":       # emit: read the needed record fields + count, write (tile u16, id u32)
-        return 4 * N + (28 + 4) * n_vis + 6 * P
-    if stage == "sort":      # read each pair once, write the sorted id once, ranges
-        return 6 * P + 4 * P + 8 * n_tiles
+    if stage == "bin":       # depth order (4 passes: key + value read and written), entry scan,
+        # level 1 (order + emission record per visible Gaussian, entries written: E <= P / 2), level 2 count
+        return 4 * N + 4 * 16 * n_vis + 8 * n_vis + (4 + 32) * n_vis + 8 * (P // 2) + 8 * n_tiles
+    if stage == "sort":      # level 2 write: read the entries, one id per pair
+        return 8 * (P // 2) + 4 * P
     if stage == "render":    # id + gathered record (36 B used) per pair, image
         return 40 * P + 12 * W * H
     raise KeyError(stage)
@@ -388,8 +389,9 @@ def run_ours(args):
             "render_work": {"E_pix": mean(E_pix), "E_blend": mean(E_blend), "E_cta": mean(E_cta),
                             "E_kept_after_warp_cull": mean(E_kept), "pixels": W * H},
             "roofline": roof,
-            # ours per frame: preprocess 1, bin 4 depth passes + emit, finalize 1, tile passes, render 1
-            "gpu_launches": n_timed * (1 + 5 + 1 + (1 if rz.layout.tile_bits <= 8 else 2) + 1),
+            # ours per frame: k_preprocess, 4 x k_onesweep, k_entry_scan, k_l1_count, k_l1_scan,
+            # k_l1_emit, k_l2_count, k_l2_scan, k_l2_write, k_render
+            "gpu_launches": n_timed * 13,
             "clocks": clk,
             "e2e": e2e,
             "prune_score": score_info,

@@ -103,24 +103,23 @@ typedef struct {
  * Records of a Gaussian with >= 1 tile (written only for those):
  *   rec  (48 B, render): q0 = (x2d, y2d, a, b), q1 = (c, t, sigma, 0), q2 = (0, r, g, b)
  *        (a, b, c) = conic Sigma_2D^-1 (Eq. 10); t = 2 log(255 sigma) (Eq. 11)
- *   erec (32 B, emission, one aligned sector): e0 = (count, info, span0, span1),
- *        e1 = (span2, span3, aux0, aux1); info = nspans | inline << 8 | columns << 9; a span
- *        is first tile (16 b) | length << 16 | column-step << 31; aux = t as float64 bits
- *        (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1) (3-sigma / SnugBox).
- * Depth lives in depth_key (float bits, 0xFFFFFFFF = no tiles).  Pairs: tile ids are
- * uint16, values are Gaussian indices (uint32). */
+ *   erec (64 B, emission): e0 = (count, info, aux0, aux1), e1..e3 = super-tile entries 0..11;
+ *        info = inline << 8 | columns << 9 | AccuTile << 10 | entries << 11; an entry is
+ *        super-tile id (16 b) | mask of its 4x4 tiles << 16 (bit (y&3)*4 + (x&3)); aux = t as
+ *        float64 bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1) (3-sigma / SnugBox).
+ * Depth lives in depth_key (float bits, 0xFFFFFFFF = no tiles).  The pairs are never
+ * stored unsorted: ss_sort writes each one once, at its sorted position (Gaussian index,
+ * uint32, in sorted_value; its tile is given by ranges, its depth by depth_key). */
 typedef struct {
     size_t rec;           /* float4 [3n]  render records                                      */
-    size_t erec;          /* uint4  [2n]  emission records                                    */
+    size_t erec;          /* uint4  [4n]  emission records                                    */
     size_t depth_key;     /* uint32 [n]   float bits of depth, 0xFFFFFFFF = no tiles          */
     size_t order;         /* uint32 [n]   visible Gaussians in (depth, index) order           */
-    size_t pair_tile;     /* uint16 [capacity] emitted tile ids (depth order)                 */
-    size_t pair_value;    /* uint32 [capacity] emitted Gaussian ids                           */
     size_t sorted_value;  /* uint32 [capacity] Gaussian ids sorted by (tile, depth, index)    */
     size_t tile_count;    /* uint32 [n_tiles]                                                 */
     size_t ranges;        /* uint32 [n_tiles][2] per tile [start, end) into sorted_value      */
     size_t n_visible;     /* uint32 [1]   Gaussians with >= 1 tile                            */
-    size_t total_pairs;   /* uint32 [1]   P                                                   */
+    size_t total_pairs;   /* uint32 [1]   P (written by ss_preprocess)                        */
     size_t overflow;      /* uint32 [1]   1 iff P > capacity                                  */
     size_t scratch;       /* internal                                                         */
     size_t total_bytes;
@@ -133,24 +132,27 @@ SS_API ss_status ss_frame_layout(int32_t n, uint32_t capacity, int32_t width, in
 /* a1 -- preprocess (Sec. 3.2.1; count mode of SnugBox/AccuTile).
  * Per Gaussian: cull (Z < z_near, singular Sigma_2D; in SnugBox/AccuTile also sigma <=
  * 1/255), project mu, Sigma_3D = R S S^T R^T (Eq. 3), Sigma_2D = J W Sigma_3D W^T J^T + 0.3 I
- * (Eq. 4), conic, SH colour, t, the mode's tile rect and tile count.  Writes rec,
- * depth_key, n_visible and the depth-digit histograms.  Reads the 16 B mean_opac of every
+ * (Eq. 4), conic, SH colour, t, the mode's tile rect and tile count.  Writes rec, erec,
+ * depth_key, n_visible, total_pairs (P) and the depth-digit histograms.  Reads the 16 B mean_opac of every
  * Gaussian and the rest only for Gaussians in front of the camera. */
 SS_API ss_status ss_preprocess(const ss_scene *scene /*host*/, const ss_camera *cam /*host*/, ss_bin_mode mode,
                         const ss_frame *frame /*host*/, void *stream);
 
-/* a2+a3 -- key allocation and emission (InclusiveSum + duplicateWithKeys).
+/* a2 + a5 -- key allocation (InclusiveSum) and tile ranges (identifyTileRanges).
  * Orders the visible Gaussians by (depth bits, index) (stable LSD radix sort, 4 passes),
- * exclusive-scans their tile counts in that order (decoupled look-back), and emits one
- * (tile id, Gaussian id) pair per tile of each Gaussian -- the tile set is recomputed from
- * the stored record by the same function as the count.  Writes order, pair_tile,
- * pair_value, tile_count, total_pairs, overflow.  Requires ss_preprocess on the frame. */
+ * scans their super-tile entry counts in that order (one entry per 4x4-tile super-tile a
+ * Gaussian's tile set touches, with the mask of its tiles there; the tile set is recomputed
+ * from the stored record by the same function as the count), partitions the entries
+ * stably by super-tile and counts the pairs of every tile: writes order, tile_count, ranges
+ * (empty tiles: [0,0)) and overflow (P = total_pairs, summed by ss_preprocess, > capacity).
+ * Requires ss_preprocess on the frame. */
 SS_API ss_status ss_bin(const ss_camera *cam /*host*/, ss_bin_mode mode, const ss_frame *frame /*host*/, void *stream);
 
-/* a4+a5 -- RadixSort + identifyTileRanges.  Stable LSD radix sort of the
- * depth-ordered pairs by tile id; the result equals a stable sort of the paper's 64-bit
- * keys (tile << 32 | depth bits) emitted in Gaussian-index order.  Writes sorted_value and
- * ranges (empty tiles: [0,0)).  Requires ss_bin on the frame. */
+/* a3 + a4 -- duplicateWithKeys + RadixSort, fused: every super-tile's
+ * depth-ordered entries are split into its tiles' lists and every pair is written once, at
+ * its sorted position.  The result (sorted_value over the ranges of ss_bin) equals the
+ * paper's stable sort of the 64-bit keys (tile << 32 | depth bits) emitted in Gaussian-index
+ * order.  Writes nothing on capacity overflow.  Requires ss_bin on the frame. */
 SS_API ss_status ss_sort(const ss_frame *frame /*host*/, void *stream);
 
 /* Materialise the paper's sorted 64-bit key array (tile << 32 | float bits of depth) from

@@ -23,11 +23,12 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
 UNITS = {
     "ss_api.cu": [],
     "ss_geometry.cu": ["--fmad=false"],
+    "ss_bin.cu": ["--fmad=false"],
     "ss_sort.cu": [],
     "ss_render.cu": [],
     "ss_prune.cu": [],
 }
-HEADERS = ["ss_common.cuh"]
+HEADERS = ["ss_common.cuh", "ss_tilegeom.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

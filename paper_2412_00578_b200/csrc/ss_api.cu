@@ -20,13 +20,17 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     int bits = 1;
     while ((1 << bits) < P.n_tiles) ++bits;
     P.tile_bits = bits;
-    L->tile_passes = bits <= 8 ? 1 : 2;
     L->n = n;
     L->capacity = capacity;
     L->nblk_depth = (uint32_t)(((size_t)n + kSortTile - 1) / kSortTile);
-    L->nblk_tile = (uint32_t)(((size_t)capacity + kSortTile - 1) / kSortTile);
-    L->nblk_emit = (uint32_t)(((size_t)n + kEmitThreads - 1) / kEmitThreads);
-    const size_t N = (size_t)n, Cap = capacity, T = (size_t)P.n_tiles;
+    L->nblk_escan = (uint32_t)(((size_t)n + 8191) / 8192);
+    L->stx = (P.tiles_x + kSuperTile - 1) / kSuperTile;
+    L->sty = (P.tiles_y + kSuperTile - 1) / kSuperTile;
+    L->n_super = L->stx * L->sty;
+    L->nck_max = (uint32_t)(((size_t)capacity + kEntChunk - 1) / kEntChunk);
+    L->n_units = (uint32_t)(((size_t)capacity + kEntWarp - 1) / kEntWarp) + 1;
+    L->l2_max_blocks = (uint32_t)(((size_t)capacity + kL2BlockEntries - 1) / kL2BlockEntries) + (uint32_t)L->n_super;
+    const size_t N = (size_t)n, Cap = capacity, T = (size_t)P.n_tiles, S = (size_t)L->n_super;
     size_t off = 0;
     auto take = [&](size_t bytes) {
         const size_t o = off;
@@ -34,7 +38,7 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
         return o;
     };
     P.rec = take(48 * N);
-    P.erec = take(32 * N);
+    P.erec = take(64 * N);
     P.depth_key = take(4 * N);
     P.order = take(4 * N);
     L->dkA = take(4 * N);
@@ -42,30 +46,34 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     L->dkB = take(4 * N);
     L->dvB = take(4 * N);
     P.scratch = L->dkA;
-    P.pair_tile = take(2 * Cap);
-    L->pair_tile2 = take(2 * Cap);
-    P.pair_value = take(4 * Cap);
-    L->pair_value2 = take(4 * Cap);
+    L->gne = take(4 * N);
+    L->one = take(4 * N);
+    L->eoff = take(4 * N);
+    L->wstart = take(4 * (size_t)L->n_units);
+    L->stg = take(8 * Cap);
+    L->ent = take(8 * Cap);
+    L->bin_M = take(4 * S * (size_t)L->nck_max);
+    L->st_total = take(4 * S);
+    L->st_base = take(4 * S);
+    L->st_blk0 = take(4 * S);
+    L->l2_blocks = take(8 * (size_t)L->l2_max_blocks);
+    L->l2_BC = take(64 * (size_t)L->l2_max_blocks);
     P.sorted_value = take(4 * Cap);
     P.ranges = take(8 * T);
+    P.tile_count = take(4 * T);
+    L->tile_base = take(4 * T);
+    P.overflow = take(4);
     // ---- regions each call clears for itself (so every call is idempotent given its inputs)
     L->zero_pre = off;  // written by ss_preprocess
     P.n_visible = take(4);
+    P.total_pairs = take(4);
     L->hist_depth = take(4 * 256 * kDepthPasses);
     L->zero_pre_end = off;
     L->zero_bin = off;  // written by ss_bin
-    P.tile_count = take(4 * T);
-    P.total_pairs = take(4);
-    P.overflow = take(4);
     L->counters = take(4 * 16);
     L->lb_depth = take(4 * 256 * (size_t)L->nblk_depth * kDepthPasses);
-    L->lb_emit = take(4 * (size_t)L->nblk_emit);
+    L->lb_escan = take(4 * (size_t)L->nblk_escan);
     L->zero_bin_end = off;
-    L->zero_sort = off;  // written by ss_sort
-    L->counters_sort = take(4 * 16);
-    L->lb_tile = take(4 * 256 * (size_t)L->nblk_tile * 2);
-    L->zero_sort_end = off;
-    L->hist_tile = take(4 * 256 * 2);
     P.total_bytes = off;
     return true;
 }
@@ -158,7 +166,7 @@ ss_status ss_bin(const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMemsetAsync(at<char>(frame->ws, L.zero_bin), 0, L.zero_bin_end - L.zero_bin, st);
     if (e == cudaSuccess) e = launch_depth_sort(frame->ws, L, st);
-    if (e == cudaSuccess) e = launch_emit(cam_args(*cam, L), (int)mode, frame->ws, L, st);
+    if (e == cudaSuccess) e = launch_bin(frame->ws, L, st);
     return cuda_status(e);
 }
 
@@ -166,10 +174,7 @@ ss_status ss_sort(const ss_frame *frame, void *stream) {
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaMemsetAsync(at<char>(frame->ws, L.zero_sort), 0, L.zero_sort_end - L.zero_sort, st);
-    if (e == cudaSuccess) e = launch_tile_sort(frame->ws, L, st);
-    return cuda_status(e);
+    return cuda_status(launch_tile_write(frame->ws, L, static_cast<cudaStream_t>(stream)));
 }
 
 ss_status ss_sorted_keys(const ss_frame *frame, uint64_t *keys, void *stream) {

@@ -1,0 +1,714 @@
+// ss_bin.cu -- a2-a5 after the depth order: the stable two-level binning of the pairs by tile.
+//
+// The paper sorts one 64-bit key (tile << 32 | depth) per (tile, Gaussian) pair.
+// With the visible Gaussians already in (depth, index) order (ss_sort.cu's depth passes),
+// the sorted pair list is a STABLE partition of that sequence's pairs by tile.  It is built
+// in two levels, on the super-tile entries of ss_tilegeom.cuh (one entry per 4x4-tile
+// super-tile a Gaussian touches, with a 16-bit mask of its tiles there):
+//   k_entry_scan  InclusiveSum over the Gaussians in depth order, of their entry
+//                 counts: every entry gets a global index, so the work of the next steps
+//                 is cut into equal-size units of entries (near Gaussians cover hundreds of
+//                 super-tiles; chunks of Gaussians would be badly unbalanced).
+//   level 1       a stable counting sort of the entries by super-tile: k_l1_count (entries
+//                 per chunk and super-tile), k_l1_scan (per super-tile prefix over the
+//                 chunks; super-tile offsets), k_l1_emit (each entry written once at its
+//                 place).  Ranks come from __match_any_sync against warp-private histograms
+//                 in shared memory: no atomics per entry.
+//   level 2       per super-tile, its depth-ordered entries are split into its 16 tile
+//                 lists with ballots on the mask bits: k_l2_count (pairs per tile; the last
+//                 CTA scans the tiles: ranges = identifyTileRanges, P.175), k_l2_write
+//                 (every pair written once, at its sorted position: duplicateWithKeys and
+//                 RadixSort fused).
+// The result is exactly the paper's stable sort of keys emitted in Gaussian-index order:
+// tiles in row-major order, each tile's Gaussians in (depth, index) order.
+#include "ss_tilegeom.cuh"
+
+namespace ss {
+namespace {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 32;
+constexpr int kScanTile = kScanThreads * kScanItems;  // Gaussians per entry-scan tile
+constexpr int kL2Threads = 256;
+constexpr int kL2PerThread = 8;
+constexpr int kL2Block = kL2Threads * kL2PerThread;  // entries per level-2 block
+static_assert(kL2Block == kL2BlockEntries, "level-2 block size");
+
+// ---------------------------------------------------------------- entry scan
+// Warp-cooperative decoupled look-back over block tickets: lane l inspects the status of
+// tile (bid - 1 - l - 32 j); the walk stops at the nearest inclusive prefix.  Returns the
+// exclusive prefix of tile bid.  Called by one full warp.
+__device__ __forceinline__ uint32_t warp_lookback(const uint32_t *lookback, uint32_t bid, int lane) {
+    const volatile uint32_t *lb = lookback;
+    uint32_t acc = 0;
+    int base = (int)bid - 1;
+    for (;;) {
+        const int idx = base - lane;
+        uint32_t v;
+        int first_inc;
+        for (;;) {  // spin until every status up to the nearest inclusive one is published
+            v = idx >= 0 ? lb[idx] : kFlagInc;  // before tile 0: a virtual inclusive 0
+            const uint32_t inc = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagInc);
+            const uint32_t zero = __ballot_sync(0xffffffffu, (v & ~kValMask) == 0);
+            first_inc = inc ? __ffs(inc) - 1 : 32;
+            const uint32_t need = first_inc == 32 ? 0xffffffffu : (0xffffffffu >> (31 - first_inc));
+            if (!(zero & need)) break;
+        }
+        uint32_t part = (lane <= first_inc) ? (v & kValMask) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        acc += part;
+        if (first_inc < 32) return acc;
+        base -= 32;
+    }
+}
+
+// eoff[k] = sum of one[0..k) over the nv visible Gaussians in depth order; total E; the
+// first Gaussian of every level-1 warp unit (wstart[b] = the Gaussian holding entry
+// b * kEntWarp); the overflow flag (P, summed by ss_preprocess, > capacity).
+__global__ void __launch_bounds__(kScanThreads) k_entry_scan(const uint32_t *__restrict__ n_visible,
+                                                             const uint32_t *__restrict__ one,
+                                                             uint32_t *__restrict__ eoff, uint32_t *__restrict__ wstart,
+                                                             uint32_t *lookback, uint32_t *ticket,
+                                                             const uint32_t *__restrict__ total_pairs, uint32_t cap,
+                                                             uint32_t *__restrict__ total_entries,
+                                                             uint32_t *__restrict__ overflow) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ uint32_t s_bid, s_base;
+    const uint32_t nv = *n_visible;
+    const int tid = threadIdx.x, lane = tid & 31;
+    if (blockIdx.x == 0 && tid == 0) *overflow = *total_pairs > cap ? 1u : 0u;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) s_bid = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint32_t bid = s_bid;
+        const size_t base = (size_t)bid * kScanTile;
+        if (base >= nv) break;
+        const size_t k0 = base + (size_t)tid * kScanItems;
+        uint32_t v[kScanItems];
+        uint32_t sum = 0;
+        if (k0 + kScanItems <= nv) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(one + k0);
+#pragma unroll
+            for (int q = 0; q < kScanItems / 4; ++q) {
+                const uint4 x = src[q];
+                v[4 * q] = x.x;
+                v[4 * q + 1] = x.y;
+                v[4 * q + 2] = x.z;
+                v[4 * q + 3] = x.w;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < kScanItems; ++q) v[q] = k0 + q < nv ? one[k0 + q] : 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < kScanItems; ++q) sum += v[q];
+        uint32_t total;
+        uint32_t run = block_exclusive_scan_256(sum, s_warp, total);
+        if (tid < 32) {
+            if (tid == 0) {
+                volatile uint32_t *lbv = lookback;
+                lbv[bid] = (bid == 0 ? kFlagInc : kFlagAgg) | total;
+            }
+            const uint32_t acc = bid == 0 ? 0u : warp_lookback(lookback, bid, lane);
+            if (tid == 0) {
+                if (bid > 0) {
+                    volatile uint32_t *lbv = lookback;
+                    lbv[bid] = kFlagInc | (acc + total);
+                }
+                s_base = acc;
+                if (base + kScanTile >= nv) *total_entries = acc + total;
+            }
+        }
+        __syncthreads();
+        run += s_base;
+#pragma unroll
+        for (int q = 0; q < kScanItems; ++q) {
+            const size_t k = k0 + q;
+            if (k < nv) {
+                eoff[k] = run;
+                // warp units whose first entry falls in this Gaussian's entries
+                for (uint32_t b = (run + kEntWarp - 1) / kEntWarp; (size_t)b * kEntWarp < (size_t)run + v[q]; ++b)
+                    wstart[b] = (uint32_t)k;
+            }
+            run += v[q];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- level 1
+struct WarpEnt {
+    uint32_t st[kEntWarp];
+    uint32_t gid[kEntWarp];
+    uint16_t mask[kEntWarp];
+};
+
+__device__ __forceinline__ void put_entry(WarpEnt &W, uint32_t e, uint32_t B0, uint32_t B1, uint32_t st,
+                                          uint32_t g, uint32_t mask) {
+    if (e >= B0 && e < B1) {
+        W.st[e - B0] = st;
+        W.gid[e - B0] = g;
+        W.mask[e - B0] = (uint16_t)mask;
+    }
+}
+
+// Entries of a Gaussian with at most kInlineEnt entries: copied from its emission record.
+__device__ __forceinline__ void inline_entries(WarpEnt &W, uint32_t g, uint32_t eo, uint32_t B0, uint32_t B1,
+                                               uint32_t ne, const uint4 &e1, const uint4 &e2, const uint4 &e3) {
+    const uint32_t v[kInlineEnt] = {e1.x, e1.y, e1.z, e1.w, e2.x, e2.y, e2.z, e2.w, e3.x, e3.y, e3.z, e3.w};
+#pragma unroll
+    for (int q = 0; q < kInlineEnt; ++q)
+        if ((uint32_t)q < ne) put_entry(W, eo + q, B0, B1, v[q] & 0xFFFFu, g, v[q] >> 16);
+}
+
+// Entries of a Gaussian with more than kInlineEnt entries, by the whole warp: lane l takes
+// bands first + l, first + l + 32, ... (AccuTile: each band's lines re-evaluated by
+// sweep_band exactly as the count evaluated them; rects: the rect's rows); a warp scan of
+// the bands' entry counts keeps the count's order.  Warp-uniform arguments.
+__device__ __noinline__ void big_entries(WarpEnt &W, uint32_t g, uint32_t eo, uint32_t B0, uint32_t B1,
+                                            uint32_t info, uint32_t aux0, uint32_t aux1,
+                                            const float4 *__restrict__ rec, int tiles_x, int tiles_y, int stx) {
+    const int lane = threadIdx.x & 31;
+    const bool accu = (info & kInfoAccuTile) != 0;
+    Sweep w;
+    int s0, s1;
+    uint32_t rect_iv = 0;
+    if (accu) {
+        const float4 q0 = rec[3 * (size_t)g + 0];
+        const float c = rec[3 * (size_t)g + 1].x;
+        const double t = __hiloint2double((int)aux1, (int)aux0);
+        accutile_setup((double)q0.x, (double)q0.y, (double)q0.z, (double)q0.w, (double)c, t, tiles_x, tiles_y, w);
+        s0 = w.s0;
+        s1 = w.s1;
+    } else {  // packed rect (x0, x1-x0-1, y0, y1-y0-1): rows y0..y1-1, each [x0, x1)
+        const int x0 = (int)(aux0 & 0xFF), x1 = x0 + (int)((aux0 >> 8) & 0xFF) + 1;
+        s0 = (int)((aux0 >> 16) & 0xFF);
+        s1 = s0 + (int)(aux0 >> 24) + 1;
+        rect_iv = (uint32_t)x0 | ((uint32_t)x1 << 16);
+        w.rows = true;
+    }
+    const bool cols = !w.rows;
+    const int b_first = s0 >> 2, b_last = (s1 - 1) >> 2;
+    uint32_t base = eo;
+    for (int bb = b_first; bb <= b_last; bb += 32) {
+        const int band = bb + lane;
+        uint32_t iv0 = 0, iv1 = 0, iv2 = 0, iv3 = 0;
+        if (band <= b_last) {
+            if (accu) {
+                sweep_band(w, band, iv0, iv1, iv2, iv3);
+            } else {
+                const int r0 = 4 * band;
+                iv0 = (r0 >= s0 && r0 < s1) ? rect_iv : 0u;
+                iv1 = (r0 + 1 >= s0 && r0 + 1 < s1) ? rect_iv : 0u;
+                iv2 = (r0 + 2 >= s0 && r0 + 2 < s1) ? rect_iv : 0u;
+                iv3 = (r0 + 3 >= s0 && r0 + 3 < s1) ? rect_iv : 0u;
+            }
+        }
+        uint32_t cnt = 0;
+        if (band <= b_last) band_entries(band, iv0, iv1, iv2, iv3, cols, stx, [&](uint32_t, uint32_t) { ++cnt; });
+        uint32_t x = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        uint32_t e = base + x - cnt;
+        if (band <= b_last)
+            band_entries(band, iv0, iv1, iv2, iv3, cols, stx,
+                         [&](uint32_t st, uint32_t mask) { put_entry(W, e++, B0, B1, st, g, mask); });
+        base += __shfl_sync(0xffffffffu, x, 31);
+    }
+}
+
+// Stages the entries [B0, B1) of warp unit b in the warp's buffer (canonical order).  The
+// unit's Gaussians are wstart[b] .. wstart[b+1] (the last may start at B1 exactly); the
+// loads of the next step of 32 Gaussians are issued before the current step is staged.
+__device__ __forceinline__ void stage_unit(WarpEnt &W, uint32_t b, uint32_t B0, uint32_t B1, uint32_t E, uint32_t nv,
+                                           const uint32_t *__restrict__ wstart, const uint32_t *__restrict__ eoff,
+                                           const uint32_t *__restrict__ order, const uint4 *__restrict__ erec,
+                                           const float4 *__restrict__ rec, int tiles_x, int tiles_y, int stx) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t k0 = wstart[b];
+    const uint32_t k1 = B1 < E ? wstart[b + 1] + 1 : nv;  // one past the unit's last Gaussian
+    struct Step {
+        uint32_t g, eo;
+        uint4 e0, e1, e2, e3;
+        bool act;
+    };
+    auto load = [&](uint32_t kb, Step &S) {
+        const uint32_t kk = kb + lane;
+        S.act = kk < k1;
+        S.eo = 0;
+        S.g = 0;
+        S.e0 = S.e1 = S.e2 = S.e3 = make_uint4(0u, 0u, 0u, 0u);
+        if (S.act) {
+            S.eo = eoff[kk];
+            S.g = order[kk];
+            const uint4 *er = erec + 4 * (size_t)S.g;  // 64 B emission record
+            S.e0 = er[0];
+            S.e1 = er[1];
+            S.e2 = er[2];
+            S.e3 = er[3];
+        }
+    };
+    Step cur, nxt;
+    load(k0, cur);
+    for (uint32_t kb = k0; kb < k1; kb += 32) {
+        if (kb + 32 < k1) load(kb + 32, nxt);
+        const bool inl = (cur.e0.y & 0x100u) != 0;
+        if (cur.act && inl) inline_entries(W, cur.g, cur.eo, B0, B1, cur.e0.y >> kInfoEntShift, cur.e1, cur.e2, cur.e3);
+        uint32_t big = __ballot_sync(0xffffffffu, cur.act && !inl);
+        while (big) {
+            const int src = __ffs(big) - 1;
+            big &= big - 1;
+            big_entries(W, __shfl_sync(0xffffffffu, cur.g, src), __shfl_sync(0xffffffffu, cur.eo, src), B0, B1,
+                        __shfl_sync(0xffffffffu, cur.e0.y, src), __shfl_sync(0xffffffffu, cur.e0.z, src),
+                        __shfl_sync(0xffffffffu, cur.e0.w, src), rec, tiles_x, tiles_y, stx);
+        }
+        cur = nxt;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void unit_bounds(uint32_t c, int w, uint32_t E, uint32_t &b, uint32_t &B0, uint32_t &B1) {
+    b = c * kBinWarps + (uint32_t)w;
+    B0 = b * (uint32_t)kEntWarp;
+    B1 = min(E, B0 + (uint32_t)kEntWarp);
+}
+
+// Lanes holding the same key (nbits wide) as this lane, by nbits ballots; 0 for invalid lanes.
+__device__ __forceinline__ uint32_t key_peers(uint32_t key, bool valid, int nbits) {
+    uint32_t peers = __ballot_sync(0xffffffffu, valid);
+    for (int bit = 0; bit < nbits; ++bit) {
+        const bool v = (key >> bit) & 1u;
+        const uint32_t m = __ballot_sync(0xffffffffu, v);
+        peers &= v ? m : ~m;
+    }
+    return valid ? peers : 0u;
+}
+
+// Per-warp histogram of the staged entries' super-tiles (leaders of the peer groups).
+__device__ __forceinline__ void unit_count(const WarpEnt &W, uint32_t n, uint32_t *h, int sbits) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (uint32_t i = 0; i < n; i += 32) {
+        const bool valid = i + lane < n;
+        const uint32_t st = valid ? W.st[i + lane] : 0u;
+        const uint32_t peers = key_peers(st, valid, sbits);
+        if (valid && (peers & lt_mask) == 0) h[st] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+// Stages every warp unit's entries once (-> stg, in entry order) and counts the entries per
+// (chunk, super-tile) -> M[c][s].
+__global__ void __launch_bounds__(kBinWarps * 32) k_l1_count(const uint32_t *__restrict__ n_visible,
+                                                              const uint32_t *__restrict__ total_entries,
+                                                              const uint32_t *__restrict__ overflow,
+                                                              const uint32_t *__restrict__ wstart,
+                                                              const uint32_t *__restrict__ eoff,
+                                                              const uint32_t *__restrict__ order,
+                                                              const uint4 *__restrict__ erec,
+                                                              const float4 *__restrict__ rec, int tiles_x, int tiles_y,
+                                                              int stx, int n_super, int sbits,
+                                                              uint32_t *__restrict__ M, uint2 *__restrict__ stg) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    WarpEnt *bufs = reinterpret_cast<WarpEnt *>(smem_raw);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(bufs + kBinWarps);
+    const uint32_t E = *total_entries, c = blockIdx.x;
+    if (*overflow || c * (uint32_t)kEntChunk >= E) return;
+    const int w = threadIdx.x >> 5;
+    for (int s = threadIdx.x; s < kBinWarps * n_super; s += blockDim.x) hist[s] = 0;
+    __syncthreads();
+    uint32_t b, B0, B1;
+    unit_bounds(c, w, E, b, B0, B1);
+    if (B0 < B1) {
+        WarpEnt &W = bufs[w];
+        stage_unit(W, b, B0, B1, E, *n_visible, wstart, eoff, order, erec, rec, tiles_x, tiles_y, stx);
+        unit_count(W, B1 - B0, hist + (size_t)w * n_super, sbits);
+        for (uint32_t i = threadIdx.x & 31; i < B1 - B0; i += 32)  // the staged entries, for k_l1_emit
+            stg[B0 + i] = make_uint2(W.gid[i], W.st[i] | ((uint32_t)W.mask[i] << 16));
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < n_super; s += blockDim.x) {
+        uint32_t sum = 0;
+#pragma unroll
+        for (int q = 0; q < kBinWarps; ++q) sum += hist[(size_t)q * n_super + s];
+        M[(size_t)c * n_super + s] = sum;
+    }
+}
+
+// Per super-tile s (one CTA): exclusive prefix of M[.][s] over the chunks, the total.  The
+// last CTA to finish scans the totals into the super-tiles' first entries and cuts every
+// super-tile's entries into level-2 blocks of at most kL2Block entries: blocks[i] =
+// (super-tile, first entry within it); st_blk0[s] = the first block of super-tile s.
+__global__ void __launch_bounds__(256) k_l1_scan(const uint32_t *__restrict__ total_entries,
+                                                 const uint32_t *__restrict__ overflow, int n_super,
+                                                 uint32_t *__restrict__ M, uint32_t *__restrict__ st_total,
+                                                 uint32_t *__restrict__ st_base, uint32_t *__restrict__ st_blk0,
+                                                 uint2 *__restrict__ blocks, uint32_t *__restrict__ n_blocks,
+                                                 uint32_t *done) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ bool s_last;
+    if (*overflow) return;
+    const uint32_t nck = (*total_entries + kEntChunk - 1) / kEntChunk;
+    const int s = blockIdx.x, tid = threadIdx.x;
+    constexpr int kPer = 8;  // chunks per thread per round, loads issued together
+    uint32_t carry = 0;
+    for (uint32_t cb = 0; cb < nck; cb += 256 * kPer) {
+        uint32_t x[kPer];
+        uint32_t local = 0;
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const uint32_t c = cb + (uint32_t)tid * kPer + q;
+            x[q] = c < nck ? M[(size_t)c * n_super + s] : 0u;
+            local += x[q];
+        }
+        uint32_t total;
+        uint32_t run = carry + block_exclusive_scan_256(local, s_warp, total);
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const uint32_t c = cb + (uint32_t)tid * kPer + q;
+            if (c < nck) M[(size_t)c * n_super + s] = run;
+            run += x[q];
+        }
+        carry += total;
+        __syncthreads();
+    }
+    if (tid == 0) st_total[s] = carry;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(done, 1u) == (uint32_t)n_super - 1u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int pers = (n_super + 255) / 256;
+    const int s0 = min(n_super, tid * pers), s1 = min(n_super, s0 + pers);
+    uint32_t le = 0, lb = 0;
+    for (int q = s0; q < s1; ++q) {
+        const uint32_t t = ((volatile uint32_t *)st_total)[q];
+        le += t;
+        lb += (t + kL2Block - 1) / kL2Block;
+    }
+    uint32_t tot_e, tot_b;
+    uint32_t re = block_exclusive_scan_256(le, s_warp, tot_e);
+    __syncthreads();  // s_warp is reused by the next scan
+    uint32_t rb = block_exclusive_scan_256(lb, s_warp, tot_b);
+    for (int q = s0; q < s1; ++q) {
+        const uint32_t t = ((volatile uint32_t *)st_total)[q];
+        st_base[q] = re;
+        st_blk0[q] = rb;
+        for (uint32_t o = 0; o < t; o += kL2Block) blocks[rb++] = make_uint2((uint32_t)q, o);
+        re += t;
+    }
+    if (tid == 0) *n_blocks = tot_b;
+}
+
+// Every entry written once, at st_base[s] + (entries of s in earlier chunks) + (in earlier
+// warps of the chunk) + its rank in the warp; the entries come from k_l1_count's staging.
+__global__ void __launch_bounds__(kBinWarps * 32) k_l1_emit(const uint32_t *__restrict__ total_entries,
+                                                             const uint32_t *__restrict__ overflow, int n_super,
+                                                             int sbits, const uint32_t *__restrict__ M,
+                                                             const uint32_t *__restrict__ st_base,
+                                                             const uint2 *__restrict__ stg, uint2 *__restrict__ ent) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw);
+    const uint32_t E = *total_entries, c = blockIdx.x;
+    if (*overflow || c * (uint32_t)kEntChunk >= E) return;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    for (int s = threadIdx.x; s < kBinWarps * n_super; s += blockDim.x) hist[s] = 0;
+    uint32_t b, B0, B1;
+    unit_bounds(c, w, E, b, B0, B1);
+    const uint32_t n = B0 < B1 ? B1 - B0 : 0u;
+    constexpr int kPerLane = kEntWarp / 32;
+    uint2 v[kPerLane];
+#pragma unroll
+    for (int q = 0; q < kPerLane; ++q) {
+        const uint32_t i = (uint32_t)q * 32 + lane;
+        v[q] = i < n ? stg[B0 + i] : make_uint2(0u, 0u);
+    }
+    __syncthreads();
+    uint32_t *h = hist + (size_t)w * n_super;
+#pragma unroll
+    for (int q = 0; q < kPerLane; ++q) {
+        const bool valid = (uint32_t)q * 32 + lane < n;
+        const uint32_t st = valid ? (v[q].y & 0xFFFFu) : 0u;
+        const uint32_t peers = key_peers(st, valid, sbits);
+        if (valid && (peers & lt_mask) == 0) h[st] += __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int s = threadIdx.x; s < n_super; s += blockDim.x) {
+        uint32_t run = st_base[s] + M[(size_t)c * n_super + s];
+#pragma unroll
+        for (int q = 0; q < kBinWarps; ++q) {
+            const uint32_t x = hist[(size_t)q * n_super + s];
+            hist[(size_t)q * n_super + s] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kPerLane; ++q) {
+        const bool valid = (uint32_t)q * 32 + lane < n;
+        const uint32_t st = valid ? (v[q].y & 0xFFFFu) : 0u;
+        const uint32_t peers = key_peers(st, valid, sbits);
+        uint32_t prev = 0;
+        if (valid) {
+            prev = h[st];
+            ent[prev + __popc(peers & lt_mask)] = make_uint2(v[q].x, v[q].y >> 16);
+        }
+        __syncwarp();
+        if (valid && (peers & lt_mask) == 0) h[st] = prev + __popc(peers);
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------- level 2
+__device__ __forceinline__ int tile_of(int s, int bit, int stx, int tiles_x) {
+    const int sy = s / stx, sx = s - sy * stx;
+    return (sy * kSuper + (bit >> 2)) * tiles_x + sx * kSuper + (bit & 3);
+}
+
+__device__ __forceinline__ bool tile_in_grid(int s, int bit, int stx, int tiles_x, int tiles_y) {
+    const int sy = s / stx, sx = s - sy * stx;
+    return sx * kSuper + (bit & 3) < tiles_x && sy * kSuper + (bit >> 2) < tiles_y;
+}
+
+// Loads the block's entries (kL2PerThread per thread, all issued together).
+__device__ __forceinline__ uint32_t l2_load(const uint2 *__restrict__ ent, uint32_t e0, uint32_t n, uint2 *v) {
+#pragma unroll
+    for (int q = 0; q < kL2PerThread; ++q) {
+        const uint32_t i = (uint32_t)q * kL2Threads + threadIdx.x;
+        v[q] = i < n ? ent[e0 + i] : make_uint2(0u, 0u);
+    }
+    return n;
+}
+
+// Pairs per tile in each level-2 block (16 ballots per 32 entries) -> BC[blk][16].
+__global__ void __launch_bounds__(kL2Threads) k_l2_count(const uint32_t *__restrict__ overflow, int stx,
+                                                         int tiles_x, int tiles_y, int n_super,
+                                                         const uint32_t *__restrict__ st_total,
+                                                         const uint32_t *__restrict__ st_base,
+                                                         const uint32_t *__restrict__ st_blk0,
+                                                         const uint2 *__restrict__ blocks,
+                                                         const uint32_t *__restrict__ n_blocks,
+                                                         const uint2 *__restrict__ ent, uint32_t *__restrict__ BC) {
+    __shared__ uint32_t s_cnt[kL2Threads / 32][16];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const bool ovf = *overflow != 0;
+    const uint32_t nb = ovf ? 0u : *n_blocks;
+    if (blockIdx.x < nb) {  // (every CTA of the grid; the ones past n_blocks have nothing to do)
+        const uint2 bl = blocks[blockIdx.x];
+        const uint32_t n = min((uint32_t)kL2Block, st_total[bl.x] - bl.y);
+        uint2 v[kL2PerThread];
+        l2_load(ent, st_base[bl.x] + bl.y, n, v);
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int q = 0; q < kL2PerThread; ++q) {
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const uint32_t bal = __ballot_sync(0xffffffffu, (v[q].y >> t) & 1u);
+                if (lane == t) cnt += __popc(bal);
+            }
+        }
+        if (lane < 16) s_cnt[w][lane] = cnt;
+        __syncthreads();
+        if (tid < 16) {
+            uint32_t sum = 0;
+#pragma unroll
+            for (int q = 0; q < kL2Threads / 32; ++q) sum += s_cnt[q][tid];
+            BC[(size_t)blockIdx.x * 16 + tid] = sum;
+        }
+    }
+}
+
+// Per super-tile and tile, the exclusive prefix over the super-tile's level-2 blocks (in BC)
+// and the tile totals; then the exclusive scan over the tiles in row-major order (tile_base,
+// ranges = identifyTileRanges).  Block blk's pairs of tile t start at tile_base[t] + BC[blk][t].
+__global__ void __launch_bounds__(1024) k_l2_scan(const uint32_t *__restrict__ overflow, int stx, int tiles_x,
+                                                  int tiles_y, int n_super, const uint32_t *__restrict__ st_total,
+                                                  const uint32_t *__restrict__ st_blk0, uint32_t *__restrict__ BC,
+                                                  uint32_t *__restrict__ tile_count, uint32_t *__restrict__ tile_base,
+                                                  uint2 *__restrict__ ranges) {
+    __shared__ uint32_t s_warp[32];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const bool ovf = *overflow != 0;
+    for (int j = tid; j < n_super * 16; j += 1024) {
+        const int sidx = j >> 4, bit = j & 15;
+        if (!tile_in_grid(sidx, bit, stx, tiles_x, tiles_y)) continue;
+        uint32_t tot = 0;
+        if (!ovf) {
+            const uint32_t nbs = (st_total[sidx] + kL2Block - 1) / kL2Block;
+            uint32_t *col = BC + (size_t)st_blk0[sidx] * 16 + bit;
+            for (uint32_t q0 = 0; q0 < nbs; q0 += 8) {  // eight independent loads in flight
+                uint32_t x[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) x[q] = q0 + q < nbs ? col[(size_t)(q0 + q) * 16] : 0u;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (q0 + q < nbs) col[(size_t)(q0 + q) * 16] = tot;
+                    tot += x[q];
+                }
+            }
+        }
+        tile_count[tile_of(sidx, bit, stx, tiles_x)] = tot;
+    }
+    __syncthreads();
+    const int T = tiles_x * tiles_y;
+    const int per = (T + 1023) / 1024;
+    const int t0 = min(T, tid * per), t1 = min(T, t0 + per);
+    uint32_t local = 0;
+    for (int t = t0; t < t1; ++t) local += tile_count[t];
+    uint32_t x = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+        uint32_t v = s_warp[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += y;
+        }
+        s_warp[lane] = v;
+    }
+    __syncthreads();
+    uint32_t run = (wid ? s_warp[wid - 1] : 0u) + x - local;
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t c = tile_count[t];
+        tile_base[t] = run;
+        ranges[t] = c ? make_uint2(run, run + c) : make_uint2(0u, 0u);
+        run += c;
+    }
+}
+
+// Every pair of a level-2 block written once: per chunk of 256 entries, 16 ballots per
+// warp, per-tile prefixes over the warps; pair (tile t, entry) -> BC[blk][t] + earlier pairs.
+__global__ void __launch_bounds__(kL2Threads) k_l2_write(const uint32_t *__restrict__ overflow, int stx,
+                                                         int tiles_x, int tiles_y,
+                                                         const uint32_t *__restrict__ st_total,
+                                                         const uint32_t *__restrict__ st_base,
+                                                         const uint2 *__restrict__ blocks,
+                                                         const uint32_t *__restrict__ n_blocks,
+                                                         const uint2 *__restrict__ ent,
+                                                         const uint32_t *__restrict__ BC,
+                                                         const uint32_t *__restrict__ tile_base,
+                                                         uint32_t *__restrict__ sorted_value) {
+    __shared__ uint32_t s_bal[kL2Threads / 32][16];
+    __shared__ uint32_t s_off[kL2Threads / 32][16];
+    __shared__ uint32_t s_run[16];
+    if (*overflow || blockIdx.x >= *n_blocks) return;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    const uint2 bl = blocks[blockIdx.x];
+    const uint32_t n = min((uint32_t)kL2Block, st_total[bl.x] - bl.y);
+    uint2 v[kL2PerThread];
+    l2_load(ent, st_base[bl.x] + bl.y, n, v);
+    if (tid < 16)
+        s_run[tid] = tile_in_grid((int)bl.x, tid, stx, tiles_x, tiles_y)
+                         ? BC[(size_t)blockIdx.x * 16 + tid] + tile_base[tile_of((int)bl.x, tid, stx, tiles_x)]
+                         : 0u;
+#pragma unroll
+    for (int q = 0; q < kL2PerThread; ++q) {
+        if ((uint32_t)q * kL2Threads >= n) break;
+        const uint32_t m = v[q].y;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, (m >> t) & 1u);
+            if (lane == t) s_bal[w][t] = bal;
+        }
+        __syncthreads();
+        if (tid < 16) {
+            uint32_t run = s_run[tid];
+#pragma unroll
+            for (int ww = 0; ww < kL2Threads / 32; ++ww) {
+                s_off[ww][tid] = run;
+                run += __popc(s_bal[ww][tid]);
+            }
+            s_run[tid] = run;
+        }
+        __syncthreads();
+        uint32_t mm = m;
+        while (mm) {
+            const int t = __ffs(mm) - 1;
+            mm &= mm - 1;
+            sorted_value[s_off[w][t] + __popc(s_bal[w][t] & lt_mask)] = v[q].x;
+        }
+        __syncthreads();
+    }
+}
+
+size_t l1_smem_bytes(int n_super) { return (size_t)kBinWarps * sizeof(WarpEnt) + (size_t)kBinWarps * n_super * 4; }
+
+}  // namespace
+
+cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
+    const ss_layout &P = L.pub;
+    if (P.n_tiles == 0) return cudaSuccess;
+    if (L.n == 0) {  // nothing to bin: empty ranges, no overflow
+        cudaError_t e = cudaMemsetAsync(at<char>(ws, P.ranges), 0, 8 * (size_t)P.n_tiles, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(at<char>(ws, P.tile_count), 0, 4 * (size_t)P.n_tiles, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(at<char>(ws, P.overflow), 0, 4, st);
+        return e;
+    }
+    uint32_t *ctr = at<uint32_t>(ws, L.counters);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int scan_grid = (int)L.nblk_escan < sms * 4 ? (int)L.nblk_escan : sms * 4;
+    k_entry_scan<<<scan_grid > 0 ? scan_grid : 1, kScanThreads, 0, st>>>(
+        at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, L.one), at<uint32_t>(ws, L.eoff),
+        at<uint32_t>(ws, L.wstart), at<uint32_t>(ws, L.lb_escan), ctr + 4, at<const uint32_t>(ws, P.total_pairs),
+        L.capacity, ctr + 8, at<uint32_t>(ws, P.overflow));
+    if (L.nck_max == 0) return cudaGetLastError();
+    const size_t smem = l1_smem_bytes(L.n_super);
+    cudaError_t e = cudaFuncSetAttribute(k_l1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const uint32_t *E = ctr + 8;
+    int sbits = 1;
+    while ((1 << sbits) < L.n_super) ++sbits;
+    k_l1_count<<<L.nck_max, kBinWarps * 32, smem, st>>>(
+        at<const uint32_t>(ws, P.n_visible), E, at<const uint32_t>(ws, P.overflow), at<const uint32_t>(ws, L.wstart),
+        at<const uint32_t>(ws, L.eoff), at<const uint32_t>(ws, P.order), at<const uint4>(ws, P.erec),
+        at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y, L.stx, L.n_super, sbits, at<uint32_t>(ws, L.bin_M),
+        at<uint2>(ws, L.stg));
+    k_l1_scan<<<L.n_super, 256, 0, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, at<uint32_t>(ws, L.bin_M),
+                                         at<uint32_t>(ws, L.st_total), at<uint32_t>(ws, L.st_base),
+                                         at<uint32_t>(ws, L.st_blk0), at<uint2>(ws, L.l2_blocks), ctr + 11, ctr + 9);
+    const size_t smem_e = (size_t)kBinWarps * L.n_super * 4;
+    e = cudaFuncSetAttribute(k_l1_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
+    if (e != cudaSuccess) return e;
+    k_l1_emit<<<L.nck_max, kBinWarps * 32, smem_e, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
+                                                         at<const uint32_t>(ws, L.bin_M),
+                                                         at<const uint32_t>(ws, L.st_base),
+                                                         at<const uint2>(ws, L.stg), at<uint2>(ws, L.ent));
+    k_l2_count<<<L.l2_max_blocks, kL2Threads, 0, st>>>(
+        at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super, at<const uint32_t>(ws, L.st_total),
+        at<const uint32_t>(ws, L.st_base), at<const uint32_t>(ws, L.st_blk0), at<const uint2>(ws, L.l2_blocks),
+        ctr + 11, at<const uint2>(ws, L.ent), at<uint32_t>(ws, L.l2_BC));
+    k_l2_scan<<<1, 1024, 0, st>>>(at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super,
+                                  at<const uint32_t>(ws, L.st_total), at<const uint32_t>(ws, L.st_blk0),
+                                  at<uint32_t>(ws, L.l2_BC), at<uint32_t>(ws, P.tile_count),
+                                  at<uint32_t>(ws, L.tile_base), at<uint2>(ws, P.ranges));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tile_write(void *ws, const Layout &L, cudaStream_t st) {
+    const ss_layout &P = L.pub;
+    if (P.n_tiles == 0 || L.n == 0 || L.capacity == 0) return cudaSuccess;
+    uint32_t *ctr = at<uint32_t>(ws, L.counters);
+    k_l2_write<<<L.l2_max_blocks, kL2Threads, 0, st>>>(
+        at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, at<const uint32_t>(ws, L.st_total),
+        at<const uint32_t>(ws, L.st_base), at<const uint2>(ws, L.l2_blocks), ctr + 11, at<const uint2>(ws, L.ent),
+        at<const uint32_t>(ws, L.l2_BC), at<const uint32_t>(ws, L.tile_base), at<uint32_t>(ws, P.sorted_value));
+    return cudaGetLastError();
+}
+
+}  // namespace ss

@@ -20,13 +20,20 @@ struct CamArgs {
     int tiles_x, tiles_y;
 };
 
-// Radix-sort geometry (shared by the sort launchers and the layout).
+// Depth-sort geometry (onesweep LSD radix sort).
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys per block tile
-constexpr int kEmitThreads = 256;                      // one Gaussian per thread
-constexpr int kInlineSpans = 4;                        // spans stored in the emission record
+constexpr int kInlineEnt = 12;                         // super-tile entries stored in the emission record
+constexpr int kLaneRows = 6;                           // AccuTile lines a preprocess lane sweeps alone
 constexpr int kDepthPasses = 4;                        // 32-bit depth keys, 8-bit digits
+constexpr uint32_t kInfoAccuTile = 0x400u;             // erec info bit: spans follow Algorithm 1
+constexpr int kInfoEntShift = 11;                      // erec info bits 11..31: super-tile entries
+constexpr int kSuperTile = 4;                          // super-tile side in tiles (ss_tilegeom.cuh)
+constexpr int kEntWarp = 256;                          // entries per warp unit of level 1
+constexpr int kBinWarps = 8;                           // warps per level-1 CTA
+constexpr int kEntChunk = kEntWarp * kBinWarps;        // entries per level-1 chunk (CTA)
+constexpr int kL2BlockEntries = 2048;                  // entries per level-2 block (CTA)
 
 // Look-back status words: 2-bit flag | 30-bit count.
 constexpr uint32_t kFlagAgg = 1u << 30;
@@ -36,22 +43,29 @@ constexpr uint32_t kValMask = (1u << 30) - 1;
 // Workspace layout (internal part beyond ss_layout).
 struct Layout {
     ss_layout pub;
-    // scratch sub-buffers
     size_t dkA, dvA, dkB, dvB;      // depth sort ping-pong (uint32 [n])
-    size_t pair_tile2;              // uint16 [capacity] tile-sort ping-pong
-    size_t pair_value2;             // uint32 [capacity]
-    size_t zero_pre, zero_pre_end;    // regions each call clears for itself
+    size_t gne;                     // uint32 [n] super-tile entries per Gaussian (index order)
+    size_t one;                     // uint32 [n] the same in depth order
+    size_t eoff;                    // uint32 [n] exclusive scan of `one`: first entry of each Gaussian
+    size_t wstart;                  // uint32 [n_units] first Gaussian of each level-1 warp unit
+    size_t stg;                     // uint2 [capacity] staged entries (Gaussian, super-tile | mask << 16)
+    size_t ent;                     // uint2 [capacity] entries (Gaussian, tile mask) by super-tile
+    size_t bin_M;                   // uint32 [nck_max][n_super] entries per (chunk, super-tile) -> prefix
+    size_t st_total, st_base;       // uint32 [n_super] entries per super-tile, first entry
+    size_t st_blk0;                 // uint32 [n_super] first level-2 block of each super-tile
+    size_t l2_blocks;               // uint2 [l2_max_blocks] (super-tile, first entry) of each block
+    size_t l2_BC;                   // uint32 [l2_max_blocks][16] pairs per (block, tile) -> prefix
+    size_t tile_base;               // uint32 [n_tiles] first sorted position of each tile
+    size_t zero_pre, zero_pre_end;  // regions each call clears for itself
     size_t zero_bin, zero_bin_end;
-    size_t zero_sort, zero_sort_end;
-    size_t counters_sort;             // uint32 [16] tile-sort tickets / barrier / sort_n
     size_t hist_depth;              // uint32 [4][256]
-    size_t hist_tile;               // uint32 [2][256]
-    size_t counters;                // uint32 [16] block tickets
+    size_t counters;                // uint32 [16] tickets: depth passes, scans, last-CTA counters
     size_t lb_depth;                // uint32 [4][nblk_depth][256]
-    size_t lb_tile;                 // uint32 [2][nblk_tile][256]
-    size_t lb_emit;                 // uint32 [nblk_emit]
-    uint32_t nblk_depth, nblk_tile, nblk_emit;
-    int tile_passes;
+    size_t lb_escan;                // uint32 [nblk_escan] look-back of the entry scan
+    uint32_t nblk_depth, nblk_escan;
+    uint32_t nck_max, n_units;      // level-1 chunks / warp units for `capacity` entries
+    uint32_t l2_max_blocks;         // level-2 blocks for `capacity` entries
+    int stx, sty, n_super;          // super-tile grid
     int32_t n;
     uint32_t capacity;
 };
@@ -67,8 +81,8 @@ __host__ __device__ inline T *at(void *ws, size_t off) {
 cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, void *ws, const Layout &L,
                               cudaStream_t st);
 cudaError_t launch_depth_sort(void *ws, const Layout &L, cudaStream_t st);
-cudaError_t launch_emit(const CamArgs &cam, int mode, void *ws, const Layout &L, cudaStream_t st);
-cudaError_t launch_tile_sort(void *ws, const Layout &L, cudaStream_t st);
+cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st);     // entry scan, level 1, tile counts
+cudaError_t launch_tile_write(void *ws, const Layout &L, cudaStream_t st);
 cudaError_t launch_sorted_keys(void *ws, const Layout &L, uint64_t *keys, cudaStream_t st);
 cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2, float *out_rgb,
                           float *out_T, uint32_t *out_nc, cudaStream_t st);

@@ -8,180 +8,10 @@
 // function on the same values (R1) and are exact for the stored conic.
 //
 // P:n = /root/reference/PAPER.md line n.
-#include "ss_common.cuh"
+#include "ss_tilegeom.cuh"
 
 namespace ss {
 namespace {
-
-// ---------------------------------------------------------------- tile geometry (float64)
-// R8: "dividing by tile size, rounding, and clipping to the image boundary":
-// half-open span [floor(lo/16), floor(hi/16)+1) clipped to [0, tiles].
-__device__ __forceinline__ void edge_span(double lo, double hi, int tiles, int &s0, int &s1) {
-    double f0 = floor(lo / kTile), f1 = floor(hi / kTile) + 1.0;
-    if (!(f0 > 0.0)) f0 = 0.0;
-    if (!(f1 > 0.0)) f1 = 0.0;
-    if (f0 > tiles) f0 = tiles;
-    if (f1 > tiles) f1 = tiles;
-    s0 = (int)f0;
-    s1 = (int)f1;
-}
-
-// SnugBox (Sec. 4.1.1, Eqs. 15-16): exact bbox of a xd^2 + 2b xd yd + c yd^2 = t (Eq. 14);
-// half-extents sqrt(t c / D), sqrt(t a / D), D = ac - b^2.  Tangent points (R11).
-struct Snug {
-    double hx, hy;   // half-extents sqrt(t c / D), sqrt(t a / D)
-    double xmin, xmax, ymin, ymax;
-    double yl, yr;   // y of the x_min / x_max tangent points (B_l, B_r)
-    double xt, xb;   // x of the y_min / y_max tangent points (B_t, B_b)
-};
-
-__device__ __forceinline__ Snug snugbox(double mx, double my, double a, double b, double c, double t) {
-    // contract R1: one reciprocal each of D, a and c; quotients are products with them
-    double D = a * c - b * b;
-    double rD = 1.0 / D;
-    double hx = sqrt(t * c * rD);
-    double hy = sqrt(t * a * rD);
-    double ia = 1.0 / a, ic = 1.0 / c;
-    Snug s;
-    s.hx = hx;
-    s.hy = hy;
-    s.xmin = mx - hx;
-    s.xmax = mx + hx;
-    s.ymin = my - hy;
-    s.ymax = my + hy;
-    s.yl = my + b * hx * ic;
-    s.yr = my - b * hx * ic;
-    s.xt = mx + b * hy * ia;
-    s.xb = mx - b * hy * ia;
-    return s;
-}
-
-__device__ __forceinline__ int4 rect_of_snug(const Snug &s, int tiles_x, int tiles_y) {
-    int4 r;
-    edge_span(s.xmin, s.xmax, tiles_x, r.x, r.y);
-    edge_span(s.ymin, s.ymax, tiles_y, r.z, r.w);
-    return r;
-}
-
-// 3D-GS baseline (Eq. 8): r = ceil(3 sqrt(lambda_max)), square mu +- r (R6, R7).
-__device__ __forceinline__ int4 rect_3sigma(double mx, double my, double cxx, double cxy, double cyy, int tiles_x,
-                                            int tiles_y) {
-    double m = 0.5 * (cxx + cyy);
-    double det = cxx * cyy - cxy * cxy;
-    double disc = m * m - det;
-    if (disc < 0.0) disc = 0.0;
-    double lmax = m + sqrt(disc);
-    double r = ceil(3.0 * sqrt(lmax));
-    int4 R;
-    edge_span(mx - r, mx + r, tiles_x, R.x, R.y);
-    edge_span(my - r, my + r, tiles_y, R.z, R.w);
-    return R;
-}
-
-// Eq. 15 on a line of the swept axis: u = (-b v +- sqrt((b^2 - a_f c_s) v^2 + t a_f)) / a_f.
-__device__ __forceinline__ void intersect_line(double m_free, double m_line, double a_free, double b, double c_line,
-                                               double t, double line, double &lo, double &hi) {
-    double v = line - m_line;
-    double disc = (b * b - a_free * c_line) * v * v + t * a_free;
-    if (disc < 0.0) disc = 0.0;  // R12
-    double s = sqrt(disc);
-    double ia = 1.0 / a_free;
-    lo = m_free + (-b * v - s) * ia;
-    hi = m_free + (-b * v + s) * ia;
-}
-
-// AccuTile, Algorithm 1 along the shorter side of the SnugBox tile rect (R9),
-// the columns path by the a<->c / x<->y swap.  R10: a boundary line outside the
-// bbox yields the neutral pair (+inf, -inf).
-struct Sweep {
-    bool rows;                                        // rows path (else columns)
-    double mf, ms, af, cs, b, t;                      // free/swept-axis centre and coefficients
-    double ext_lo, ext_hi, smin, smax, tmin_s, tmax_s;
-    int s0, s1, f0, f1;                               // swept lines [s0, s1), free span [f0, f1)
-};
-
-__device__ __forceinline__ bool accutile_setup_from(const Snug &S, const int4 &R, double mx, double my, double a,
-                                                    double b, double c, double t, Sweep &w) {
-    if (R.x >= R.y || R.z >= R.w) return false;
-    w.rows = (R.w - R.z) <= (R.y - R.x);
-    w.b = b;
-    w.t = t;
-    if (w.rows) {
-        w.mf = mx; w.ms = my; w.af = a; w.cs = c;
-        w.ext_lo = S.xmin; w.ext_hi = S.xmax; w.smin = S.ymin; w.smax = S.ymax;
-        w.tmin_s = S.yl; w.tmax_s = S.yr;
-        w.s0 = R.z; w.s1 = R.w; w.f0 = R.x; w.f1 = R.y;
-    } else {
-        w.mf = my; w.ms = mx; w.af = c; w.cs = a;
-        w.ext_lo = S.ymin; w.ext_hi = S.ymax; w.smin = S.xmin; w.smax = S.xmax;
-        w.tmin_s = S.xt; w.tmax_s = S.xb;
-        w.s0 = R.x; w.s1 = R.y; w.f0 = R.z; w.f1 = R.w;
-    }
-    return true;
-}
-
-__device__ __forceinline__ bool accutile_setup(double mx, double my, double a, double b, double c, double t,
-                                               int tiles_x, int tiles_y, Sweep &w) {
-    const Snug S = snugbox(mx, my, a, b, c, t);
-    const int4 R = rect_of_snug(S, tiles_x, tiles_y);
-    return accutile_setup_from(S, R, mx, my, a, b, c, t, w);
-}
-
-// Intersections(line, E) or the neutral pair when the algorithm does not compute it.
-__device__ __forceinline__ void sweep_line(const Sweep &w, double line, bool compute, double &lo, double &hi) {
-    lo = __longlong_as_double(0x7ff0000000000000ll);   // +inf
-    hi = __longlong_as_double(0xfff0000000000000ll);   // -inf
-    if (compute) intersect_line(w.mf, w.ms, w.af, w.b, w.cs, w.t, line, lo, hi);
-}
-
-// One row (or column) r of Algorithm 1 given i_min (its lower boundary line) and i_max (its
-// upper boundary line): e_min / e_max, Convert, clip to the rect.  Returns [tmin, tmax).
-__device__ __forceinline__ void sweep_row(const Sweep &w, int r, double imin_lo, double imin_hi, double imax_lo,
-                                          double imax_hi, int &tmin, int &tmax) {
-    const double lo_r = (double)(r * kTile), hi_r = (double)((r + 1) * kTile);
-    const double e_min = (w.tmin_s >= lo_r && w.tmin_s < hi_r) ? w.ext_lo : (imin_lo < imax_lo ? imin_lo : imax_lo);
-    const double e_max = (w.tmax_s >= lo_r && w.tmax_s < hi_r) ? w.ext_hi : (imin_hi > imax_hi ? imin_hi : imax_hi);
-    double g0 = floor(e_min / kTile), g1 = floor(e_max / kTile) + 1.0;
-    if (!(g0 > w.f0)) g0 = w.f0;
-    if (g0 > w.f1) g0 = w.f1;
-    if (!(g1 > w.f0)) g1 = w.f0;
-    if (g1 > w.f1) g1 = w.f1;
-    tmin = (int)g0;
-    tmax = (int)g1;
-}
-
-// Algorithm 1 in count mode on a prepared sweep (same loop as the sequential form below).
-// One span (row or column of the sweep) packed in 32 bits: first tile id (16 bits), length
-// (bits 16..24, <= 256), column-step flag (bit 31: consecutive tiles are tiles_x apart).
-__device__ __forceinline__ uint32_t pack_span(const Sweep &w, int r, int tmin, int tmax, int tiles_x) {
-    const uint32_t len = tmax > tmin ? (uint32_t)(tmax - tmin) : 0u;
-    const uint32_t first = len == 0 ? 0u : (w.rows ? (uint32_t)(r * tiles_x + tmin) : (uint32_t)(tmin * tiles_x + r));
-    return first | (len << 16) | (w.rows ? 0u : 0x80000000u);
-}
-
-// Algorithm 1 in count mode on a prepared sweep (the sequential loop, i_min <- i_max); the
-// first kInlineSpans spans are also returned packed (for the emission record).
-__device__ __forceinline__ uint32_t accutile_count(const Sweep &w, int tiles_x, uint32_t *spans) {
-    uint32_t C = 0;
-    double imin_lo, imin_hi;
-    const double line_min = (double)(w.s0 * kTile);
-    sweep_line(w, line_min, line_min >= w.smin, imin_lo, imin_hi);
-    for (int r = w.s0; r < w.s1; ++r) {
-        double imax_lo, imax_hi;
-        const double line_max = (double)((r + 1) * kTile);
-        sweep_line(w, line_max, line_max <= w.smax, imax_lo, imax_hi);
-        int tmin, tmax;
-        sweep_row(w, r, imin_lo, imin_hi, imax_lo, imax_hi, tmin, tmax);
-        if (tmax > tmin) C += (uint32_t)(tmax - tmin);
-        const int j = r - w.s0;
-#pragma unroll
-        for (int q = 0; q < kInlineSpans; ++q)
-            if (j == q) spans[q] = pack_span(w, r, tmin, tmax, tiles_x);
-        imin_lo = imax_lo;
-        imin_hi = imax_hi;
-    }
-    return C;
-}
 
 // ---------------------------------------------------------------- SH basis (R13)
 template <int DEG>
@@ -217,24 +47,31 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
                                                     const float4 *__restrict__ scale, const float4 *__restrict__ rot,
                                                     const float4 *__restrict__ sh, CamArgs cam, int mode,
                                                     float4 *__restrict__ rec, uint4 *__restrict__ erec,
-                                                    uint32_t *__restrict__ depth_key, uint32_t *__restrict__ hist,
-                                                    uint32_t *__restrict__ n_visible) {
+                                                    uint32_t *__restrict__ depth_key, uint32_t *__restrict__ gne,
+                                                    uint32_t *__restrict__ hist,
+                                                    uint32_t *__restrict__ n_visible,
+                                                    uint32_t *__restrict__ total_pairs) {
     __shared__ uint32_t s_hist[kDepthPasses][256];
-    __shared__ uint32_t s_vis;
+    __shared__ uint32_t s_vis, s_pairs;
     for (int k = threadIdx.x; k < kDepthPasses * 256; k += blockDim.x) (&s_hist[0][0])[k] = 0;
-    if (threadIdx.x == 0) s_vis = 0;
+    if (threadIdx.x == 0) s_vis = s_pairs = 0;
     __syncthreads();
     constexpr int NB = (DEG + 1) * (DEG + 1);
     constexpr int NP = (NB * 3 + 3) / 4;
-    uint32_t my_vis = 0;
+    uint32_t my_vis = 0, my_pairs = 0;
     // camera constants of the J clamp (R5), the same values the per-Gaussian form would give
     const float limx = cam.clip * ((0.5f * (float)cam.W) / cam.fx);
     const float limy = cam.clip * ((0.5f * (float)cam.H) / cam.fy);
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int stx = (cam.tiles_x + kSuper - 1) / kSuper;
+    const int lane = threadIdx.x & 31;
+    // warp-uniform grid-stride loop (the tall-Gaussian phase below is warp-collective)
+    for (int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += gridDim.x * blockDim.x) {
+        const int i = i0 + lane;
+        const bool valid = i < n;
         uint32_t count = 0;
-        const float4 mo = mean_opac[i];
-        const float4 q4 = rot[i];    // issued with the mean: one memory round trip, not two
-        const float4 s4 = scale[i];
+        const float4 mo = valid ? mean_opac[i] : make_float4(0.f, 0.f, -1.f, 0.f);
+        const float4 q4 = valid ? rot[i] : make_float4(1.f, 0.f, 0.f, 0.f);  // issued with the mean
+        const float4 s4 = valid ? scale[i] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float px = cam.V[0] * mo.x + cam.V[1] * mo.y + cam.V[2] * mo.z + cam.V[3];
         const float py = cam.V[4] * mo.x + cam.V[5] * mo.y + cam.V[6] * mo.z + cam.V[7];
         const float pz = cam.V[8] * mo.x + cam.V[9] * mo.y + cam.V[10] * mo.z + cam.V[11];
@@ -243,9 +80,15 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
         int4 R = make_int4(0, 0, 0, 0);
         Snug snug;
         snug.hx = snug.hy = 0.0;
-        uint32_t spans[kInlineSpans] = {0u, 0u, 0u, 0u};
-        uint32_t nspans = 0, cols = 0;
-        if (pz >= cam.z_near) {
+        uint32_t cols = 0, n_ent = 0;
+        bool tall = false;       // AccuTile with more than kLaneRows lines: the warp-collective phase
+        // entries go straight to the emission record (only Gaussians with tiles get one)
+        uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 4 * (size_t)i) + 4;
+        auto put = [&](uint32_t st, uint32_t mask) {
+            if (n_ent < (uint32_t)kInlineEnt) ent_out[n_ent] = st | (mask << 16);
+            ++n_ent;
+        };
+        if (valid && pz >= cam.z_near) {
             const float iz = 1.0f / pz;  // contract R1: one reciprocal of z
             const float tx = px * iz, ty = py * iz;
             x2d = cam.fx * tx + cam.cx;
@@ -310,19 +153,82 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
                         Sweep w;
                         if (accutile_setup_from(snug, R, (double)x2d, (double)y2d, (double)a, (double)b, (double)c,
                                                 td, w)) {
-                            count = accutile_count(w, cam.tiles_x, spans);
-                            nspans = (uint32_t)(w.s1 - w.s0);
                             cols = w.rows ? 0u : 1u;
+                            if (w.s1 - w.s0 <= kLaneRows) {
+                                EntryAcc acc;
+                                acc_init(acc, !w.rows, stx);
+                                count = accutile_count(w, cam.tiles_x,
+                                                       [&](int r, int lo, int hi) { acc_feed(acc, r, lo, hi, put); });
+                                acc_flush(acc, put);
+                            } else {
+                                tall = true;
+                            }
                         }
                     } else if (R.x < R.y && R.z < R.w) {
                         count = (uint32_t)((R.y - R.x) * (R.w - R.z));
-                        nspans = (uint32_t)(R.w - R.z);
+                        // super-tile entries of the rect: its super-tile rect, masks of the overlap
+                        for (int band = R.z >> 2; band <= (R.w - 1) >> 2; ++band) {
+                            uint32_t rows = 0;
 #pragma unroll
-                        for (int q = 0; q < kInlineSpans; ++q)
-                            if (q < (int)nspans)
-                                spans[q] = (uint32_t)((R.z + q) * cam.tiles_x + R.x) | ((uint32_t)(R.y - R.x) << 16);
+                            for (int q = 0; q < 4; ++q)
+                                rows |= (4 * band + q >= R.z && 4 * band + q < R.w) ? (1u << (4 * q)) : 0u;
+                            for (int C = R.x >> 2; C <= (R.y - 1) >> 2; ++C) {
+                                const int x0 = max(R.x, 4 * C), x1 = min(R.y, 4 * C + 4);
+                                const uint32_t cb = ((1u << (x1 - x0)) - 1u) << (x0 - 4 * C);
+                                put((uint32_t)(band * stx + C), rows * cb);
+                            }
+                        }
                     }
                 }
+            }
+        }
+        // Tall Gaussians, one at a time by the whole warp (bounded divergence): lane l takes
+        // bands first + l, ... of 4 lines, each evaluated by sweep_band exactly as the sequential
+        // loop evaluates them; pairs and entries are summed over the warp, entries written in
+        // the count's order straight into the owner's emission record.
+        uint32_t tall_mask = __ballot_sync(0xffffffffu, tall);
+        while (tall_mask) {
+            const int src = __ffs(tall_mask) - 1;
+            tall_mask &= tall_mask - 1;
+            const int gi = __shfl_sync(0xffffffffu, i, src);
+            const float bx = __shfl_sync(0xffffffffu, x2d, src), by = __shfl_sync(0xffffffffu, y2d, src);
+            const float ba = __shfl_sync(0xffffffffu, a, src), bb = __shfl_sync(0xffffffffu, b, src);
+            const float bc = __shfl_sync(0xffffffffu, c, src);
+            const double bt = __hiloint2double(__shfl_sync(0xffffffffu, __double2hiint(td), src),
+                                               __shfl_sync(0xffffffffu, __double2loint(td), src));
+            Sweep w;
+            accutile_setup((double)bx, (double)by, (double)ba, (double)bb, (double)bc, bt, cam.tiles_x, cam.tiles_y,
+                           w);
+            uint32_t pairs = 0, ents = 0;
+            uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 4 * (size_t)gi) + 4;
+            const int last = (w.s1 - 1) >> 2;
+            for (int b0 = w.s0 >> 2; b0 <= last; b0 += 32) {
+                const int band = b0 + lane;
+                uint32_t iv0 = 0, iv1 = 0, iv2 = 0, iv3 = 0;
+                if (band <= last) sweep_band(w, band, iv0, iv1, iv2, iv3);
+                auto len = [](uint32_t v) { return (v >> 16) > (v & 0xFFFFu) ? (v >> 16) - (v & 0xFFFFu) : 0u; };
+                uint32_t p = len(iv0) + len(iv1) + len(iv2) + len(iv3);
+                uint32_t ne = 0;
+                if (band <= last) band_entries(band, iv0, iv1, iv2, iv3, !w.rows, stx, [&](uint32_t, uint32_t) { ++ne; });
+                uint32_t x = ne;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                    p += __shfl_xor_sync(0xffffffffu, p, o);
+                }
+                uint32_t j = ents + x - ne;
+                if (band <= last)
+                    band_entries(band, iv0, iv1, iv2, iv3, !w.rows, stx, [&](uint32_t st, uint32_t mask) {
+                        if (j < (uint32_t)kInlineEnt) ent_out[j] = st | (mask << 16);
+                        ++j;
+                    });
+                ents += __shfl_sync(0xffffffffu, x, 31);
+                pairs += p;
+            }
+            if (lane == src) {
+                count = pairs;
+                n_ent = ents;
             }
         }
         if (count > 0) {
@@ -359,9 +265,11 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             q[0] = make_float4(x2d, y2d, a, b);
             q[1] = make_float4(c, (float)td, mo.w, 0.0f);
             q[2] = make_float4(0.0f, rgb0, rgb1, rgb2);
-            // emission record (32 B, one sector): e0 (count, info, span0, span1), e1 (span2, span3,
-            // aux0, aux1); info = nspans | inline flag << 8 | columns flag << 9; aux = t as float64
-            // bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1) for the fallback path.
+            // emission record (64 B): e0 (count, info, aux0, aux1), e1..e3 = entries 0..11 (written
+            // as they were found; the words past the entry count are stale);
+            // info = inline flag << 8 | columns flag << 9 | AccuTile flag << 10 | entries << 11;
+            // aux = t as float64 bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1)
+            // for the re-enumeration of Gaussians with more than kInlineEnt entries.
             uint32_t aux0, aux1;
             if (mode == SS_BIN_ACCUTILE) {
                 aux0 = (uint32_t)__double2loint(td);
@@ -371,261 +279,40 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
                        ((uint32_t)(R.w - R.z - 1) << 24);
                 aux1 = 0u;
             }
-            const uint32_t info = nspans | (nspans <= (uint32_t)kInlineSpans ? 0x100u : 0u) | (cols << 9);
-            erec[2 * (size_t)i + 0] = make_uint4(count, info, spans[0], spans[1]);
-            erec[2 * (size_t)i + 1] = make_uint4(spans[2], spans[3], aux0, aux1);
+            const uint32_t info = (n_ent <= (uint32_t)kInlineEnt ? 0x100u : 0u) | (cols << 9) |
+                                  (mode == SS_BIN_ACCUTILE ? kInfoAccuTile : 0u) | (n_ent << kInfoEntShift);
+            uint4 *er = erec + 4 * (size_t)i;
+            er[0] = make_uint4(count, info, aux0, aux1);
             const uint32_t key = __float_as_uint(pz);
             depth_key[i] = key;
+            gne[i] = n_ent;
 #pragma unroll
             for (int p = 0; p < kDepthPasses; ++p) atomicAdd(&s_hist[p][(key >> (8 * p)) & 0xFF], 1u);
             ++my_vis;
-        } else {
+            my_pairs += count;
+        } else if (valid) {
             depth_key[i] = kNoTiles;
+            gne[i] = 0u;
         }
     }
     // warp-aggregate the visible count, then one atomic per CTA
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) my_vis += __shfl_xor_sync(0xffffffffu, my_vis, o);
-    if ((threadIdx.x & 31) == 0 && my_vis) atomicAdd(&s_vis, my_vis);
+    for (int o = 16; o > 0; o >>= 1) {
+        my_vis += __shfl_xor_sync(0xffffffffu, my_vis, o);
+        my_pairs += __shfl_xor_sync(0xffffffffu, my_pairs, o);
+    }
+    if ((threadIdx.x & 31) == 0 && my_vis) {
+        atomicAdd(&s_vis, my_vis);
+        atomicAdd(&s_pairs, my_pairs);
+    }
     __syncthreads();
     for (int k = threadIdx.x; k < kDepthPasses * 256; k += blockDim.x) {
         const uint32_t v = (&s_hist[0][0])[k];
         if (v) atomicAdd(hist + k, v);
     }
-    if (threadIdx.x == 0 && s_vis) atomicAdd(n_visible, s_vis);
-}
-
-// ---------------------------------------------------------------- a2+a3 emission kernel
-// A CTA takes 256 consecutive visible Gaussians in (depth, index) order.
-//  1. Their tile counts are exclusive-scanned across the grid (block scan + decoupled
-//     look-back over block tickets assigned in launch order): the CTA's pairs occupy
-//     [base, base + total) in Gaussian order.
-//  2. Each thread runs the row (or column) loop of its Gaussian -- the same arithmetic as the
-//     count of a1 (AccuTile: Algorithm 1 with the i_min <- i_max carry; 3-sigma / SnugBox: the
-//     rect's rows) -- and stores one span (first tile, length, step, Gaussian) per row in
-//     shared memory.  At most kSpanCap spans per round; threads that do not fit go next round.
-//  3. The CTA flattens the spans (scan of lengths) and writes pair p of the round at
-//     base + round_base + p, so the global writes are contiguous and every thread writes the
-//     same number of pairs regardless of Gaussian size.  A per-CTA tile histogram in shared
-//     memory feeds the tile sort and the ranges.
-constexpr int kSpanCap = 2048;
-constexpr int kEmitBlock = kEmitThreads;
-
-// Warp-cooperative decoupled look-back: lane l inspects the status of CTA (bid - 1 - l - 32j);
-// the walk stops at the nearest inclusive prefix; aggregates before it are summed.  Returns
-// the exclusive prefix of CTA bid.  Called by one full warp.
-__device__ __forceinline__ uint32_t warp_lookback(const uint32_t *lookback, uint32_t bid, int lane) {
-    const volatile uint32_t *lb = lookback;
-    uint32_t acc = 0;
-    int base = (int)bid - 1;
-    for (;;) {
-        const int idx = base - lane;
-        uint32_t v;
-        int first_inc;
-        uint32_t need;
-        for (;;) {  // spin until every status up to the nearest inclusive one is published
-            v = idx >= 0 ? lb[idx] : kFlagInc;  // before CTA 0: a virtual inclusive 0
-            const uint32_t inc = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagInc);
-            const uint32_t zero = __ballot_sync(0xffffffffu, (v & ~kValMask) == 0);
-            first_inc = inc ? __ffs(inc) - 1 : 32;
-            need = first_inc == 32 ? 0xffffffffu : (0xffffffffu >> (31 - first_inc));
-            if (!(zero & need)) break;
-        }
-        uint32_t part = (lane <= first_inc) ? (v & kValMask) : 0u;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        acc += part;
-        if (first_inc < 32) return acc;
-        base -= 32;
-    }
-}
-
-// Exclusive scan over the first 256 threads of a kEmitBlock CTA (the look-back warp passes 0
-// and ignores the result); every thread of the CTA must call it.
-__device__ __forceinline__ uint32_t emit_scan(uint32_t v, uint32_t *s_warp, uint32_t &total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t x = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31 && wid < 8) s_warp[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        uint32_t w = lane < 8 ? s_warp[lane] : 0u;
-#pragma unroll
-        for (int o = 1; o < 8; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        if (lane < 8) s_warp[lane] = w;
-    }
-    __syncthreads();
-    total = s_warp[7];
-    return (wid && wid < 8 ? s_warp[wid - 1] : 0u) + x - v;
-}
-
-__global__ void __launch_bounds__(kEmitBlock, 3) k_emit(int mode, const float4 *__restrict__ rec,
-                                                        const uint4 *__restrict__ erec,
-                                                        const uint32_t *__restrict__ order,
-                                                        const uint32_t *__restrict__ n_visible, uint32_t cap,
-                                                        uint16_t *__restrict__ pair_tile,
-                                                        uint32_t *__restrict__ pair_value, uint32_t *tile_count,
-                                                        uint32_t *lookback, uint32_t *ticket,
-                                                        uint32_t *total_pairs, uint32_t *overflow, int tiles_x,
-                                                        int tiles_y, int n_tiles, int smem_hist) {
-    extern __shared__ uint32_t s_tile_hist[];
-    __shared__ uint32_t s_span[kSpanCap];  // first tile | len << 16 | column-step flag << 31
-    __shared__ uint32_t s_gid[kSpanCap];
-    __shared__ uint32_t s_pfx[kSpanCap];   // exclusive prefix of span lengths within the round
-    __shared__ uint32_t s_warp[8];
-    __shared__ uint32_t s_bid, s_base, s_nspans;
-    const bool lb_warp = threadIdx.x >= kEmitThreads;
-    const int lane = threadIdx.x & 31;
-    for (int t = threadIdx.x; t < (smem_hist ? n_tiles : 0); t += blockDim.x) s_tile_hist[t] = 0;
-    const uint32_t nv = *n_visible;
-    uint32_t *hist = smem_hist ? s_tile_hist : tile_count;
-    for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_bid = atomicAdd(ticket, 1u);
-        __syncthreads();
-        const uint32_t bid = s_bid;
-        if ((size_t)bid * kEmitThreads >= nv) break;
-        const uint32_t k = bid * kEmitThreads + threadIdx.x;
-        uint32_t g = 0, cnt = 0;
-        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;
-        if (!lb_warp && k < nv) {
-            g = order[k];
-            e0 = erec[2 * (size_t)g + 0];  // one aligned 32 B sector per Gaussian
-            e1 = erec[2 * (size_t)g + 1];
-            cnt = e0.x;
-        }
-        uint32_t total;
-        emit_scan(cnt, s_warp, total);
-        const uint32_t ns = cnt ? (e0.y & 0xFFu) : 0u;
-        const bool inline_spans = (e0.y & 0x100u) != 0;
-        if (threadIdx.x == 0) lookback[bid] = (bid == 0 ? kFlagInc : kFlagAgg) | total;
-        bool first_round = true;
-        // warp 0: decoupled look-back (run after its span generation, so that predecessors have
-        // had time to publish), the inclusive prefix, and P for the last CTA
-        auto emit_lookback_publish = [&]() {
-            const uint32_t acc = bid == 0 ? 0u : warp_lookback(lookback, bid, lane);
-            if (lane == 0) {
-                if (bid > 0) {
-                    volatile uint32_t *lbv = lookback;
-                    lbv[bid] = kFlagInc | (acc + total);
-                }
-                s_base = acc;
-                if ((bid + 1) * kEmitThreads >= nv) {
-                    *total_pairs = acc + total;
-                    *overflow = acc + total > cap ? 1u : 0u;
-                }
-            }
-        };
-        bool pending = ns > 0;
-        uint32_t round_base = 0;  // pairs of this CTA written in previous rounds
-        while (__syncthreads_or(pending)) {
-            uint32_t span_tot;
-            const uint32_t sofs = emit_scan(pending ? ns : 0u, s_warp, span_tot);
-            const bool take = pending && sofs + ns <= (uint32_t)kSpanCap;
-            // spans taken this round: all, or up to the first thread that does not fit
-            if (threadIdx.x == 0 && span_tot <= (uint32_t)kSpanCap) s_nspans = span_tot;
-            if (pending && sofs <= (uint32_t)kSpanCap && sofs + ns > (uint32_t)kSpanCap) s_nspans = sofs;
-            if (take) {
-                uint32_t j = sofs;
-                if (inline_spans) {  // spans recorded by ss_preprocess's count
-                    const uint32_t sp[kInlineSpans] = {e0.z, e0.w, e1.x, e1.y};
-#pragma unroll
-                    for (int q = 0; q < kInlineSpans; ++q)
-                        if (q < (int)ns) {
-                            s_span[j + q] = sp[q];
-                            s_gid[j + q] = g;
-                        }
-                } else if (mode == SS_BIN_ACCUTILE) {  // rare: more rows than inline slots
-                    const float4 q0 = rec[3 * (size_t)g + 0];
-                    const float c = rec[3 * (size_t)g + 1].x;
-                    const double t = __hiloint2double((int)e1.w, (int)e1.z);
-                    Sweep w;
-                    accutile_setup((double)q0.x, (double)q0.y, (double)q0.z, (double)q0.w, (double)c, t, tiles_x,
-                                   tiles_y, w);
-                    double imin_lo, imin_hi;
-                    const double line_min = (double)(w.s0 * kTile);
-                    sweep_line(w, line_min, line_min >= w.smin, imin_lo, imin_hi);
-                    for (int r = w.s0; r < w.s1; ++r, ++j) {
-                        double imax_lo, imax_hi;
-                        const double line_max = (double)((r + 1) * kTile);
-                        sweep_line(w, line_max, line_max <= w.smax, imax_lo, imax_hi);
-                        int tmin, tmax;
-                        sweep_row(w, r, imin_lo, imin_hi, imax_lo, imax_hi, tmin, tmax);
-                        s_span[j] = pack_span(w, r, tmin, tmax, tiles_x);
-                        s_gid[j] = g;
-                        imin_lo = imax_lo;  // i_min <- i_max
-                        imin_hi = imax_hi;
-                    }
-                } else {  // 3-sigma / SnugBox: the rect's rows
-                    const uint32_t pr = e1.z;
-                    const int x0 = (int)(pr & 0xFF), w_ = (int)((pr >> 8) & 0xFF) + 1, y0 = (int)((pr >> 16) & 0xFF);
-                    for (int r = y0; r < y0 + (int)ns; ++r, ++j) {
-                        s_span[j] = (uint32_t)(r * tiles_x + x0) | ((uint32_t)w_ << 16);
-                        s_gid[j] = g;
-                    }
-                }
-                pending = false;
-            }
-            if (first_round && threadIdx.x < 32) emit_lookback_publish();
-            first_round = false;
-            __syncthreads();
-            const uint32_t nspans = s_nspans;
-            // exclusive prefix of the span lengths (8 spans per thread of the first 256)
-            uint32_t loc[kSpanCap / kEmitThreads];
-            uint32_t my = 0;
-#pragma unroll
-            for (int q = 0; q < kSpanCap / kEmitThreads; ++q) {
-                const uint32_t jj = threadIdx.x * (kSpanCap / kEmitThreads) + q;
-                loc[q] = (!lb_warp && jj < nspans) ? (s_span[jj] >> 16) & 0x7FFFu : 0u;
-                my += loc[q];
-            }
-            uint32_t round_pairs;
-            uint32_t run = emit_scan(my, s_warp, round_pairs);
-            if (!lb_warp) {
-#pragma unroll
-                for (int q = 0; q < kSpanCap / kEmitThreads; ++q) {
-                    const uint32_t jj = threadIdx.x * (kSpanCap / kEmitThreads) + q;
-                    if (jj < nspans) s_pfx[jj] = run;
-                    run += loc[q];
-                }
-            }
-            __syncthreads();
-            // flatten (all kEmitBlock threads): pair p of the round -> last span j with s_pfx[j] <= p
-            const uint32_t out0 = s_base + round_base;
-            for (uint32_t p = threadIdx.x; p < round_pairs; p += kEmitBlock) {
-                uint32_t lo = 0, hi = nspans - 1;
-                while (lo < hi) {
-                    const uint32_t mid = (lo + hi + 1) >> 1;
-                    if (s_pfx[mid] <= p) lo = mid;
-                    else hi = mid - 1;
-                }
-                const uint32_t sp = s_span[lo];
-                const uint32_t step = (sp & 0x80000000u) ? (uint32_t)tiles_x : 1u;
-                const uint32_t tile = (sp & 0xFFFFu) + (p - s_pfx[lo]) * step;
-                const uint32_t o = out0 + p;
-                if (o < cap) {
-                    pair_tile[o] = (uint16_t)tile;
-                    pair_value[o] = s_gid[lo];
-                }
-                atomicAdd(hist + tile, 1u);
-            }
-            round_base += round_pairs;
-        }
-        if (first_round && threadIdx.x < 32) emit_lookback_publish();  // CTA without spans
-    }
-    if (smem_hist) {
-        __syncthreads();
-        for (int t = threadIdx.x; t < n_tiles; t += blockDim.x) {
-            const uint32_t v = s_tile_hist[t];
-            if (v) atomicAdd(tile_count + t, v);
-        }
+    if (threadIdx.x == 0 && s_vis) {
+        atomicAdd(n_visible, s_vis);
+        atomicAdd(total_pairs, s_pairs);
     }
 }
 
@@ -643,8 +330,8 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
 #define SS_PRE_ARGS                                                                                       \
     sc.n, reinterpret_cast<const float4 *>(sc.mean_opac), reinterpret_cast<const float4 *>(sc.scale),         \
         reinterpret_cast<const float4 *>(sc.rot), reinterpret_cast<const float4 *>(sc.sh), cam, mode,         \
-        at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key),                         \
-        at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible)
+        at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key), at<uint32_t>(ws, L.gne), \
+        at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs)
     switch (sc.sh_degree) {
         case 0: k_preprocess<0><<<grid, 256, 0, st>>>(SS_PRE_ARGS); break;
         case 1: k_preprocess<1><<<grid, 256, 0, st>>>(SS_PRE_ARGS); break;
@@ -652,26 +339,6 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
         default: k_preprocess<3><<<grid, 256, 0, st>>>(SS_PRE_ARGS); break;
     }
 #undef SS_PRE_ARGS
-    return cudaGetLastError();
-}
-
-cudaError_t launch_emit(const CamArgs &cam, int mode, void *ws, const Layout &L, cudaStream_t st) {
-    const ss_layout &P = L.pub;
-    if (P.n_tiles == 0 || L.nblk_emit == 0) return cudaSuccess;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int smem_hist = P.n_tiles <= 12288 ? 1 : 0;
-    const size_t smem = smem_hist ? (size_t)P.n_tiles * 4 : 0;
-    if (smem > 20 * 1024)  // static (~25 KB) + dynamic above the default 48 KB window
-        cudaFuncSetAttribute(k_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    const int grid = (int)L.nblk_emit < sms * 4 ? (int)L.nblk_emit : sms * 4;
-    k_emit<<<grid, kEmitBlock, smem, st>>>(
-        mode, at<const float4>(ws, P.rec), at<const uint4>(ws, P.erec), at<const uint32_t>(ws, P.order),
-        at<const uint32_t>(ws, P.n_visible), L.capacity,
-        at<uint16_t>(ws, P.pair_tile), at<uint32_t>(ws, P.pair_value), at<uint32_t>(ws, P.tile_count),
-        at<uint32_t>(ws, L.lb_emit), at<uint32_t>(ws, L.counters) + 8, at<uint32_t>(ws, P.total_pairs),
-        at<uint32_t>(ws, P.overflow), cam.tiles_x, cam.tiles_y, P.n_tiles, smem_hist);
     return cudaGetLastError();
 }
 

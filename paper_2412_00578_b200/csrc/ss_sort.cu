@@ -1,14 +1,12 @@
 // ss_sort.cu -- stable LSD radix sort (onesweep, decoupled look-back) and tile ranges.
 //
-// Used twice per frame:
-//   a2  depth order: the visible Gaussians' 32-bit depth keys, 4 x 8-bit passes; pass 0
-//       reads every Gaussian's key (implicit value = index) and drops the 0xFFFFFFFF
-//       sentinel of Gaussians without tiles (compaction fused into the first pass);
-//   a4  tile order: the uint16 tile ids of the depth-ordered pairs, 1-2 x 8-bit passes; the
-//       last pass writes only the Gaussian ids.  Stability makes the result equal to the
-//       paper's stable sort of (tile << 32 | depth) keys.
-// a5 (identifyTileRanges) is the exclusive scan of the per-tile pair counts that
-// the emission kernel histogrammed (k_tile_finalize), so no pass over the keys is needed.
+// The depth order of the visible Gaussians: their 32-bit depth keys, 4 x
+// 8-bit passes; pass 0 reads every Gaussian's key (implicit value = index) and drops the
+// 0xFFFFFFFF sentinel of Gaussians without tiles (compaction fused into the first pass).
+// The last pass also gathers each Gaussian's super-tile entry count into depth order for
+// ss_bin.cu, which partitions the depth-ordered pairs by tile (a stable two-level binning;
+// stability makes the result equal to the paper's stable sort of (tile << 32 | depth) keys,
+// P:174).
 #include "ss_common.cuh"
 
 namespace ss {
@@ -35,7 +33,9 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restric
                                                               uint32_t *__restrict__ vals_out, const uint32_t *n_ptr,
                                                               uint32_t n_fixed, int shift,
                                                               const uint32_t *__restrict__ digit_count,
-                                                              uint32_t *lookback, uint32_t *ticket) {
+                                                              uint32_t *lookback, uint32_t *ticket,
+                                                              const uint32_t *__restrict__ gather_src = nullptr,
+                                                              uint32_t *__restrict__ gather_dst = nullptr) {
     __shared__ uint32_t s_whist[kWarps][256];
     __shared__ uint32_t s_digit_base[256];
     __shared__ uint32_t s_dig_out[256];
@@ -169,59 +169,9 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restric
             const uint32_t o = s_dig_out[d] + (i - s_blk_start[d]);
             if (WRITE_KEYS) keys_out[o] = k;
             vals_out[o] = s_vals[i];
+            if (gather_dst) gather_dst[o] = gather_src[s_vals[i]];  // per-Gaussian value, depth order
         }
     }
-}
-
-// a5: ranges = exclusive scan of the per-tile pair counts; the digit histograms of the tile
-// passes; the number of pairs to sort (0 on capacity overflow).  One CTA of 1024 threads.
-__global__ void __launch_bounds__(1024) k_tile_finalize(const uint32_t *__restrict__ tile_count, int n_tiles,
-                                                        int passes, const uint32_t *total_pairs,
-                                                        const uint32_t *overflow, uint2 *__restrict__ ranges,
-                                                        uint32_t *__restrict__ hist, uint32_t *sort_n) {
-    __shared__ uint32_t s_hist[2][256];
-    __shared__ uint32_t s_warp[32];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const bool ovf = *overflow != 0;
-    for (int k = tid; k < 512; k += 1024) (&s_hist[0][0])[k] = 0;
-    __syncthreads();
-    const int per = (n_tiles + 1023) / 1024;
-    const int t0 = tid * per, t1 = min(n_tiles, t0 + per);
-    uint32_t local = 0;
-    for (int t = t0; t < t1; ++t) {
-        const uint32_t c = ovf ? 0u : tile_count[t];
-        local += c;
-        if (c) {
-            atomicAdd(&s_hist[0][t & 0xFF], c);
-            if (passes > 1) atomicAdd(&s_hist[1][(t >> 8) & 0xFF], c);
-        }
-    }
-    uint32_t x = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        uint32_t w = s_warp[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += y;
-        }
-        s_warp[lane] = w;
-    }
-    __syncthreads();
-    uint32_t run = (wid ? s_warp[wid - 1] : 0u) + x - local;
-    for (int t = t0; t < t1; ++t) {
-        const uint32_t c = ovf ? 0u : tile_count[t];
-        ranges[t] = c ? make_uint2(run, run + c) : make_uint2(0u, 0u);
-        run += c;
-    }
-    for (int k = tid; k < 512; k += 1024) hist[k] = (&s_hist[0][0])[k];
-    if (tid == 0) *sort_n = ovf ? 0u : *total_pairs;
 }
 
 // The paper's sorted key array, materialised for inspection: keys[j] = tile << 32 | depth.
@@ -263,34 +213,8 @@ cudaError_t launch_depth_sort(void *ws, const Layout &L, cudaStream_t st) {
     k_onesweep<uint32_t, false, false, true><<<grid, kSortThreads, 0, st>>>(kB, vB, kA, vA, nvis, 0, 16, hist + 512,
                                                                           lb + 2 * lbs, tick + 2);
     k_onesweep<uint32_t, false, false, false><<<grid, kSortThreads, 0, st>>>(
-        kA, vA, nullptr, at<uint32_t>(ws, P.order), nvis, 0, 24, hist + 768, lb + 3 * lbs, tick + 3);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_tile_sort(void *ws, const Layout &L, cudaStream_t st) {
-    const ss_layout &P = L.pub;
-    uint32_t *hist = at<uint32_t>(ws, L.hist_tile);
-    uint32_t *tick = at<uint32_t>(ws, L.counters);
-    uint32_t *sort_n = tick + 15;
-    k_tile_finalize<<<1, 1024, 0, st>>>(at<const uint32_t>(ws, P.tile_count), P.n_tiles, L.tile_passes,
-                                        at<const uint32_t>(ws, P.total_pairs), at<const uint32_t>(ws, P.overflow),
-                                        at<uint2>(ws, P.ranges), hist, sort_n);
-    if (L.capacity == 0) return cudaGetLastError();
-    const int grid = sort_grid(L.nblk_tile);
-    uint32_t *lb = at<uint32_t>(ws, L.lb_tile);
-    const size_t lbs = (size_t)L.nblk_tile * 256;
-    uint16_t *k0 = at<uint16_t>(ws, P.pair_tile), *k1 = at<uint16_t>(ws, L.pair_tile2);
-    uint32_t *v0 = at<uint32_t>(ws, P.pair_value), *v1 = at<uint32_t>(ws, L.pair_value2);
-    uint32_t *out = at<uint32_t>(ws, P.sorted_value);
-    if (L.tile_passes == 1) {
-        k_onesweep<uint16_t, false, false, false><<<grid, kSortThreads, 0, st>>>(k0, v0, nullptr, out, sort_n, 0, 0,
-                                                                               hist, lb, tick + 4);
-    } else {
-        k_onesweep<uint16_t, false, false, true><<<grid, kSortThreads, 0, st>>>(k0, v0, k1, v1, sort_n, 0, 0, hist,
-                                                                              lb, tick + 4);
-        k_onesweep<uint16_t, false, false, false><<<grid, kSortThreads, 0, st>>>(k1, v1, nullptr, out, sort_n, 0, 8,
-                                                                               hist + 256, lb + lbs, tick + 5);
-    }
+        kA, vA, nullptr, at<uint32_t>(ws, P.order), nvis, 0, 24, hist + 768, lb + 3 * lbs, tick + 3,
+        at<const uint32_t>(ws, L.gne), at<uint32_t>(ws, L.one));
     return cudaGetLastError();
 }
 

@@ -98,8 +98,8 @@ class Rasterizer:
         return self._view(self.layout.rec, 12 * self.scene.n, torch.float32).view(self.scene.n, 12)
 
     def emit_records(self) -> torch.Tensor:
-        """[N, 8] int32 emission records: (count, info, span0..3, aux0, aux1)."""
-        return self._view(self.layout.erec, 8 * self.scene.n, torch.int32).view(self.scene.n, 8)
+        """[N, 16] int32 emission records: (count, info, aux0, aux1, entry0..11)."""
+        return self._view(self.layout.erec, 16 * self.scene.n, torch.int32).view(self.scene.n, 16)
 
     def counts(self) -> torch.Tensor:
         """Per-Gaussian tile count of the current frame (int32, 0 for Gaussians without tiles)."""
@@ -111,12 +111,6 @@ class Rasterizer:
 
     def order(self) -> torch.Tensor:
         return self._view(self.layout.order, self.scene.n, torch.int32)
-
-    def pair_tiles(self) -> torch.Tensor:
-        return self._view(self.layout.pair_tile, self.capacity, torch.int16)
-
-    def pair_values(self) -> torch.Tensor:
-        return self._view(self.layout.pair_value, self.capacity, torch.int32)
 
     def sorted_values(self) -> torch.Tensor:
         return self._view(self.layout.sorted_value, self.capacity, torch.int32)

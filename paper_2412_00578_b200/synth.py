@@ -168,6 +168,30 @@ def tiny_scene(n=1000, seed=0, low_sigma=False, sh_degree=3) -> tuple[Scene, Cam
     return scene, cam
 
 
+def dense_scene(n=12000, seed=5, tie_frac=0.5, sh_degree=1) -> tuple[Scene, Camera]:
+    """Tile-sort stress case on the tiny camera: means packed into a 64x64 px window at the
+    image centre, so the central tiles' lists are longer than one shared-memory sort
+    (ss_sort's global-memory path), and a fraction `tie_frac` of the Gaussians share the
+    exact depth 5.0 (equal keys, ordered by index)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    W = H = 256
+    cam = look_at((0, 0, 0), (0, 0, 1), W, H, 60.0, up=(0, -1, 0))
+    fx = cam.fx
+    u = rng.uniform(96, 160, n)
+    v = rng.uniform(96, 160, n)
+    z = rng.uniform(2.0, 8.0, n)
+    z[rng.uniform(0, 1, n) < tie_frac] = 5.0
+    x = (u - cam.cx) * z / fx
+    y = (v - cam.cy) * z / fx
+    px_sigma = np.exp(rng.normal(math.log(6.0), 0.6, (n, 3))).clip(1.0, 30.0)
+    scale = px_sigma * z[:, None] / fx
+    opac = rng.uniform(0.02, 0.3, n)
+    mean_opac = np.stack([x, y, z, opac], 1).astype(np.float32)
+    sc = np.concatenate([scale, np.zeros((n, 1))], 1).astype(np.float32)
+    scene = Scene(mean_opac, sc, _haar_quaternions(rng, n), _sh_planes(rng, n, sh_degree), sh_degree, "dense")
+    return scene, cam
+
+
 def orbit_scene(n, seed, object_frac=0.6, mu_s=-5.75, sd_s=1.0, sh_degree=3, name="orbit") -> Scene:
     """SURVEY §8(d) Mip-NeRF-360-shaped 'object + unbounded background' scene."""
     rng = np.random.Generator(np.random.PCG64(seed))

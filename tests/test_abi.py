@@ -31,7 +31,7 @@ def test_layout_and_workspace(lib):
     L = _abi.layout(1000, 4096, 256, 256)
     assert (L.tiles_x, L.tiles_y, L.n_tiles, L.tile_bits) == (16, 16, 256, 8)
     assert L.total_bytes == _abi.workspace_size(1000, 4096, 256, 256)
-    offs = sorted([L.rec, L.erec, L.depth_key, L.order, L.pair_tile, L.pair_value, L.sorted_value,
+    offs = sorted([L.rec, L.erec, L.depth_key, L.order, L.sorted_value,
                    L.ranges, L.tile_count, L.n_visible, L.total_pairs, L.overflow])
     assert len(set(offs)) == len(offs) and all(o % 256 == 0 for o in offs)
     L2 = _abi.layout(10, 100, 1297, 840)
@@ -58,7 +58,8 @@ def test_invalid_arguments_rejected_before_launch(lib):
     sc3 = _abi.SsScene(10, 3, 1, 1, 1, 1)
     assert lib.ss_preprocess(C.byref(sc3), C.byref(st), 7, C.byref(fr), None) == _abi.SS_ERR_INVALID_ARG
     big = _abi.SsFrame(1234, 1 << 40, 10, 100, 16 * 65537, 16)
-    assert lib.ss_sort(C.byref(big), None) == _abi.SS_ERR_UNSUPPORTED  # > 65536 tiles
+    assert lib.ss_sort(C.byref(big), None) == _abi.SS_ERR_UNSUPPORTED  # > 256 tiles along x
+    assert _abi.layout(10, 100, 4096, 4096).n_tiles == 65536  # the largest supported grid (no launch here)
     assert lib.ss_status_string(_abi.SS_ERR_CUDA) == b"SS_ERR_CUDA"
 
 

@@ -60,11 +60,11 @@ def _check_frame(scene, cam, mode, bg=(0.0, 0.0, 0.0), capacity=None, image=True
     assert np.all(g["depth_key"][~vis] == 0xFFFFFFFF)
     er = g["erec"][vis]
     if mode == "accutile":  # aux = t as float64 bits: 2 log(255 sigma) of the stored sigma
-        t64 = er[:, 6:8].copy().view(np.float64)[:, 0]
+        t64 = er[:, 2:4].copy().view(np.float64)[:, 0]
         t_or = np.array([oracle.threshold(s) for s in orr[:, 6]])
         assert np.all(np.abs(t64 - t_or) <= 4.5e-16 * np.abs(t_or))  # CUDA log vs glibc log (R2)
     else:  # the packed tile rect
-        pr = er[:, 6]
+        pr = er[:, 2]
         x0, y0 = pr & 0xFF, (pr >> 16) & 0xFF
         rect = np.stack([x0, x0 + ((pr >> 8) & 0xFF) + 1, y0, y0 + (pr >> 24) + 1], 1)
         assert np.array_equal(rect.astype(np.int32), f.rect[vis])
@@ -101,6 +101,18 @@ def test_medium_multiblock_parity(mode):
     scene, _ = synth.make_workload("mnr360-3m", n=40000)
     cam = synth.orbit_cameras(185, 630, 470)[11]
     _check_frame(scene, cam, mode, bg=(0.1, 0.2, 0.3))
+
+
+@pytest.mark.parametrize("mode", ["3sigma", "accutile"])
+def test_dense_ties_and_long_tiles(mode):
+    """Sort stress: central tiles hold more than 4096 pairs each and half the Gaussians share
+    one depth, so equal (tile, depth) keys are frequent; they must come out in index order,
+    bit-exactly like the oracle's stable sort."""
+    scene, cam = synth.dense_scene()
+    g, f = _check_frame(scene, cam, mode)
+    lens = f.ranges[:, 1] - f.ranges[:, 0]
+    assert lens.max() > 4096
+    assert (np.diff(g["keys"]) == 0).sum() > 1000
 
 
 def test_binned_renders_equal_on_gpu():
