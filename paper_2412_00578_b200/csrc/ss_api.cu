@@ -28,7 +28,6 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     L->sty = (P.tiles_y + kSuperTile - 1) / kSuperTile;
     L->n_super = L->stx * L->sty;
     L->nck_max = (uint32_t)(((size_t)capacity + kEntChunk - 1) / kEntChunk);
-    L->n_units = (uint32_t)(((size_t)capacity + kEntWarp - 1) / kEntWarp) + 1;
     L->l2_max_blocks = (uint32_t)(((size_t)capacity + kL2BlockEntries - 1) / kL2BlockEntries) + (uint32_t)L->n_super;
     const size_t N = (size_t)n, Cap = capacity, T = (size_t)P.n_tiles, S = (size_t)L->n_super;
     size_t off = 0;
@@ -49,7 +48,6 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     L->gne = take(4 * N);
     L->one = take(4 * N);
     L->eoff = take(4 * N);
-    L->wstart = take(4 * (size_t)L->n_units);
     L->stg = take(8 * Cap);
     L->ent = take(8 * Cap);
     L->bin_M = take(4 * S * (size_t)L->nck_max);

@@ -64,11 +64,10 @@ __device__ __forceinline__ uint32_t warp_lookback(const uint32_t *lookback, uint
 }
 
 // eoff[k] = sum of one[0..k) over the nv visible Gaussians in depth order; total E; the
-// first Gaussian of every level-1 warp unit (wstart[b] = the Gaussian holding entry
-// b * kEntWarp); the overflow flag (P, summed by ss_preprocess, > capacity).
+// overflow flag (P, summed by ss_preprocess, > capacity).
 __global__ void __launch_bounds__(kScanThreads) k_entry_scan(const uint32_t *__restrict__ n_visible,
                                                              const uint32_t *__restrict__ one,
-                                                             uint32_t *__restrict__ eoff, uint32_t *__restrict__ wstart,
+                                                             uint32_t *__restrict__ eoff,
                                                              uint32_t *lookback, uint32_t *ticket,
                                                              const uint32_t *__restrict__ total_pairs, uint32_t cap,
                                                              uint32_t *__restrict__ total_entries,
@@ -126,48 +125,51 @@ __global__ void __launch_bounds__(kScanThreads) k_entry_scan(const uint32_t *__r
 #pragma unroll
         for (int q = 0; q < kScanItems; ++q) {
             const size_t k = k0 + q;
-            if (k < nv) {
-                eoff[k] = run;
-                // warp units whose first entry falls in this Gaussian's entries
-                for (uint32_t b = (run + kEntWarp - 1) / kEntWarp; (size_t)b * kEntWarp < (size_t)run + v[q]; ++b)
-                    wstart[b] = (uint32_t)k;
-            }
+            if (k < nv) eoff[k] = run;
             run += v[q];
         }
     }
 }
 
 // ---------------------------------------------------------------- level 1
-struct WarpEnt {
-    uint32_t st[kEntWarp];
-    uint32_t gid[kEntWarp];
-    uint16_t mask[kEntWarp];
-};
+// Staged entries (entry order): (Gaussian, super-tile | mask << 16).
+__device__ __forceinline__ void put_entry(uint2 *__restrict__ stg, uint32_t e, uint32_t st, uint32_t g,
+                                          uint32_t mask) {
+    stg[e] = make_uint2(g, st | (mask << 16));
+}
 
-__device__ __forceinline__ void put_entry(WarpEnt &W, uint32_t e, uint32_t B0, uint32_t B1, uint32_t st,
-                                          uint32_t g, uint32_t mask) {
-    if (e >= B0 && e < B1) {
-        W.st[e - B0] = st;
-        W.gid[e - B0] = g;
-        W.mask[e - B0] = (uint16_t)mask;
-    }
+// Entries of a Gaussian whose line spans are stored in its emission record (AccuTile, at most
+// kLaneRows lines): the band accumulator over the spans, in the count's order.
+__device__ __forceinline__ void span_entries(uint2 *__restrict__ stg, uint32_t g, uint32_t eo, uint32_t info,
+                                             const uint4 &e1, const uint4 &e2, int stx) {
+    const uint32_t v[6] = {e1.x, e1.y, e1.z, e1.w, e2.x, e2.y};
+    const uint32_t ns = info & 0xFFu;
+    EntryAcc acc;
+    acc_init(acc, (info & kInfoCols) != 0, stx);
+    uint32_t e = eo;
+    auto out = [&](uint32_t st, uint32_t mask) { put_entry(stg, e++, st, g, mask); };
+#pragma unroll
+    for (int q = 0; q < 6; ++q)
+        if ((uint32_t)q < ns)
+            acc_feed(acc, (int)(v[q] >> 18), (int)(v[q] & 0x1FFu), (int)((v[q] >> 9) & 0x1FFu), out);
+    acc_flush(acc, out);
 }
 
 // Entries of a Gaussian with at most kInlineEnt entries: copied from its emission record.
-__device__ __forceinline__ void inline_entries(WarpEnt &W, uint32_t g, uint32_t eo, uint32_t B0, uint32_t B1,
-                                               uint32_t ne, const uint4 &e1, const uint4 &e2, const uint4 &e3) {
+__device__ __forceinline__ void inline_entries(uint2 *__restrict__ stg, uint32_t g, uint32_t eo, uint32_t ne,
+                                               const uint4 &e1, const uint4 &e2, const uint4 &e3) {
     const uint32_t v[kInlineEnt] = {e1.x, e1.y, e1.z, e1.w, e2.x, e2.y, e2.z, e2.w, e3.x, e3.y, e3.z, e3.w};
 #pragma unroll
     for (int q = 0; q < kInlineEnt; ++q)
-        if ((uint32_t)q < ne) put_entry(W, eo + q, B0, B1, v[q] & 0xFFFFu, g, v[q] >> 16);
+        if ((uint32_t)q < ne) put_entry(stg, eo + q, v[q] & 0xFFFFu, g, v[q] >> 16);
 }
 
 // Entries of a Gaussian with more than kInlineEnt entries, by the whole warp: lane l takes
 // bands first + l, first + l + 32, ... (AccuTile: each band's lines re-evaluated by
 // sweep_band exactly as the count evaluated them; rects: the rect's rows); a warp scan of
 // the bands' entry counts keeps the count's order.  Warp-uniform arguments.
-__device__ __noinline__ void big_entries(WarpEnt &W, uint32_t g, uint32_t eo, uint32_t B0, uint32_t B1,
-                                            uint32_t info, uint32_t aux0, uint32_t aux1,
+__device__ __noinline__ void big_entries(uint2 *__restrict__ stg, uint32_t g, uint32_t eo, uint32_t info,
+                                            uint32_t aux0, uint32_t aux1,
                                             const float4 *__restrict__ rec, int tiles_x, int tiles_y, int stx) {
     const int lane = threadIdx.x & 31;
     const bool accu = (info & kInfoAccuTile) != 0;
@@ -189,6 +191,7 @@ __device__ __noinline__ void big_entries(WarpEnt &W, uint32_t g, uint32_t eo, ui
         w.rows = true;
     }
     const bool cols = !w.rows;
+    (void)info;
     const int b_first = s0 >> 2, b_last = (s1 - 1) >> 2;
     uint32_t base = eo;
     for (int bb = b_first; bb <= b_last; bb += 32) {
@@ -216,59 +219,51 @@ __device__ __noinline__ void big_entries(WarpEnt &W, uint32_t g, uint32_t eo, ui
         uint32_t e = base + x - cnt;
         if (band <= b_last)
             band_entries(band, iv0, iv1, iv2, iv3, cols, stx,
-                         [&](uint32_t st, uint32_t mask) { put_entry(W, e++, B0, B1, st, g, mask); });
+                         [&](uint32_t st, uint32_t mask) { put_entry(stg, e++, st, g, mask); });
         base += __shfl_sync(0xffffffffu, x, 31);
     }
 }
 
-// Stages the entries [B0, B1) of warp unit b in the warp's buffer (canonical order).  The
-// unit's Gaussians are wstart[b] .. wstart[b+1] (the last may start at B1 exactly); the
-// loads of the next step of 32 Gaussians are issued before the current step is staged.
-__device__ __forceinline__ void stage_unit(WarpEnt &W, uint32_t b, uint32_t B0, uint32_t B1, uint32_t E, uint32_t nv,
-                                           const uint32_t *__restrict__ wstart, const uint32_t *__restrict__ eoff,
-                                           const uint32_t *__restrict__ order, const uint4 *__restrict__ erec,
-                                           const float4 *__restrict__ rec, int tiles_x, int tiles_y, int stx) {
+// Every visible Gaussian's entries, in depth order, written to their global entry slots
+// stg[eoff[k] ..] (one thread per Gaussian; Gaussians with more than kInlineEnt entries by
+// the whole warp).  Warp-uniform grid-stride loop.
+__global__ void __launch_bounds__(256) k_entries(const uint32_t *__restrict__ n_visible,
+                                                 const uint32_t *__restrict__ overflow,
+                                                 const uint32_t *__restrict__ eoff, const uint32_t *__restrict__ order,
+                                                 const uint4 *__restrict__ erec, const float4 *__restrict__ rec,
+                                                 int tiles_x, int tiles_y, int stx, uint2 *__restrict__ stg) {
+    if (*overflow) return;
+    const uint32_t nv = *n_visible;
     const int lane = threadIdx.x & 31;
-    const uint32_t k0 = wstart[b];
-    const uint32_t k1 = B1 < E ? wstart[b + 1] + 1 : nv;  // one past the unit's last Gaussian
-    struct Step {
-        uint32_t g, eo;
-        uint4 e0, e1, e2, e3;
-        bool act;
-    };
-    auto load = [&](uint32_t kb, Step &S) {
-        const uint32_t kk = kb + lane;
-        S.act = kk < k1;
-        S.eo = 0;
-        S.g = 0;
-        S.e0 = S.e1 = S.e2 = S.e3 = make_uint4(0u, 0u, 0u, 0u);
-        if (S.act) {
-            S.eo = eoff[kk];
-            S.g = order[kk];
-            const uint4 *er = erec + 4 * (size_t)S.g;  // 64 B emission record
-            S.e0 = er[0];
-            S.e1 = er[1];
-            S.e2 = er[2];
-            S.e3 = er[3];
+    for (uint32_t k0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); k0 < nv; k0 += gridDim.x * blockDim.x) {
+        const uint32_t k = k0 + lane;
+        const bool act = k < nv;
+        uint32_t g = 0, eo = 0;
+        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0, e2 = e0, e3 = e0;
+        if (act) {
+            g = order[k];
+            eo = eoff[k];
+            const uint4 *er = erec + 4 * (size_t)g;  // 64 B emission record: only the words in use
+            e0 = er[0];
+            const uint32_t info = e0.y;
+            const uint32_t words = (info & kInfoSpanInline) ? (info & 0xFFu)
+                                   : (info & kInfoEntInline) ? (info >> kInfoEntShift) : 0u;
+            if (words > 0) e1 = er[1];
+            if (words > 4) e2 = er[2];
+            if (words > 8) e3 = er[3];
         }
-    };
-    Step cur, nxt;
-    load(k0, cur);
-    for (uint32_t kb = k0; kb < k1; kb += 32) {
-        if (kb + 32 < k1) load(kb + 32, nxt);
-        const bool inl = (cur.e0.y & 0x100u) != 0;
-        if (cur.act && inl) inline_entries(W, cur.g, cur.eo, B0, B1, cur.e0.y >> kInfoEntShift, cur.e1, cur.e2, cur.e3);
-        uint32_t big = __ballot_sync(0xffffffffu, cur.act && !inl);
+        const bool spn = (e0.y & kInfoSpanInline) != 0, ent = (e0.y & kInfoEntInline) != 0;
+        if (act && spn) span_entries(stg, g, eo, e0.y, e1, e2, stx);
+        if (act && ent) inline_entries(stg, g, eo, e0.y >> kInfoEntShift, e1, e2, e3);
+        uint32_t big = __ballot_sync(0xffffffffu, act && !spn && !ent);
         while (big) {
             const int src = __ffs(big) - 1;
             big &= big - 1;
-            big_entries(W, __shfl_sync(0xffffffffu, cur.g, src), __shfl_sync(0xffffffffu, cur.eo, src), B0, B1,
-                        __shfl_sync(0xffffffffu, cur.e0.y, src), __shfl_sync(0xffffffffu, cur.e0.z, src),
-                        __shfl_sync(0xffffffffu, cur.e0.w, src), rec, tiles_x, tiles_y, stx);
+            big_entries(stg, __shfl_sync(0xffffffffu, g, src), __shfl_sync(0xffffffffu, eo, src),
+                        __shfl_sync(0xffffffffu, e0.y, src), __shfl_sync(0xffffffffu, e0.z, src),
+                        __shfl_sync(0xffffffffu, e0.w, src), rec, tiles_x, tiles_y, stx);
         }
-        cur = nxt;
     }
-    __syncwarp();
 }
 
 __device__ __forceinline__ void unit_bounds(uint32_t c, int w, uint32_t E, uint32_t &b, uint32_t &B0, uint32_t &B1) {
@@ -288,47 +283,36 @@ __device__ __forceinline__ uint32_t key_peers(uint32_t key, bool valid, int nbit
     return valid ? peers : 0u;
 }
 
-// Per-warp histogram of the staged entries' super-tiles (leaders of the peer groups).
-__device__ __forceinline__ void unit_count(const WarpEnt &W, uint32_t n, uint32_t *h, int sbits) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    for (uint32_t i = 0; i < n; i += 32) {
-        const bool valid = i + lane < n;
-        const uint32_t st = valid ? W.st[i + lane] : 0u;
-        const uint32_t peers = key_peers(st, valid, sbits);
-        if (valid && (peers & lt_mask) == 0) h[st] += __popc(peers);
-        __syncwarp();
-    }
-}
-
-// Stages every warp unit's entries once (-> stg, in entry order) and counts the entries per
-// (chunk, super-tile) -> M[c][s].
-__global__ void __launch_bounds__(kBinWarps * 32) k_l1_count(const uint32_t *__restrict__ n_visible,
-                                                              const uint32_t *__restrict__ total_entries,
-                                                              const uint32_t *__restrict__ overflow,
-                                                              const uint32_t *__restrict__ wstart,
-                                                              const uint32_t *__restrict__ eoff,
-                                                              const uint32_t *__restrict__ order,
-                                                              const uint4 *__restrict__ erec,
-                                                              const float4 *__restrict__ rec, int tiles_x, int tiles_y,
-                                                              int stx, int n_super, int sbits,
-                                                              uint32_t *__restrict__ M, uint2 *__restrict__ stg) {
+// Entries per (chunk, super-tile) -> M[c][s], from the staged entries.
+__global__ void __launch_bounds__(kBinWarps * 32) k_l1_count(const uint32_t *__restrict__ total_entries,
+                                                              const uint32_t *__restrict__ overflow, int n_super,
+                                                              int sbits, const uint2 *__restrict__ stg,
+                                                              uint32_t *__restrict__ M) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    WarpEnt *bufs = reinterpret_cast<WarpEnt *>(smem_raw);
-    uint32_t *hist = reinterpret_cast<uint32_t *>(bufs + kBinWarps);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw);
     const uint32_t E = *total_entries, c = blockIdx.x;
     if (*overflow || c * (uint32_t)kEntChunk >= E) return;
-    const int w = threadIdx.x >> 5;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lt_mask = (1u << lane) - 1u;
     for (int s = threadIdx.x; s < kBinWarps * n_super; s += blockDim.x) hist[s] = 0;
-    __syncthreads();
     uint32_t b, B0, B1;
     unit_bounds(c, w, E, b, B0, B1);
-    if (B0 < B1) {
-        WarpEnt &W = bufs[w];
-        stage_unit(W, b, B0, B1, E, *n_visible, wstart, eoff, order, erec, rec, tiles_x, tiles_y, stx);
-        unit_count(W, B1 - B0, hist + (size_t)w * n_super, sbits);
-        for (uint32_t i = threadIdx.x & 31; i < B1 - B0; i += 32)  // the staged entries, for k_l1_emit
-            stg[B0 + i] = make_uint2(W.gid[i], W.st[i] | ((uint32_t)W.mask[i] << 16));
+    const uint32_t n = B0 < B1 ? B1 - B0 : 0u;
+    constexpr int kPerLane = kEntWarp / 32;
+    uint32_t st[kPerLane];
+#pragma unroll
+    for (int q = 0; q < kPerLane; ++q) {
+        const uint32_t i = (uint32_t)q * 32 + lane;
+        st[q] = i < n ? (stg[B0 + i].y & 0xFFFFu) : 0u;
+    }
+    __syncthreads();
+    uint32_t *h = hist + (size_t)w * n_super;
+#pragma unroll
+    for (int q = 0; q < kPerLane; ++q) {
+        const bool valid = (uint32_t)q * 32 + lane < n;
+        const uint32_t peers = key_peers(st[q], valid, sbits);
+        if (valid && (peers & lt_mask) == 0) h[st[q]] += __popc(peers);
+        __syncwarp();
     }
     __syncthreads();
     for (int s = threadIdx.x; s < n_super; s += blockDim.x) {
@@ -645,7 +629,7 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_write(const uint32_t *__restr
     }
 }
 
-size_t l1_smem_bytes(int n_super) { return (size_t)kBinWarps * sizeof(WarpEnt) + (size_t)kBinWarps * n_super * 4; }
+size_t l1_smem_bytes(int n_super) { return (size_t)kBinWarps * n_super * 4; }
 
 }  // namespace
 
@@ -665,27 +649,26 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
     const int scan_grid = (int)L.nblk_escan < sms * 4 ? (int)L.nblk_escan : sms * 4;
     k_entry_scan<<<scan_grid > 0 ? scan_grid : 1, kScanThreads, 0, st>>>(
         at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, L.one), at<uint32_t>(ws, L.eoff),
-        at<uint32_t>(ws, L.wstart), at<uint32_t>(ws, L.lb_escan), ctr + 4, at<const uint32_t>(ws, P.total_pairs),
-        L.capacity, ctr + 8, at<uint32_t>(ws, P.overflow));
+        at<uint32_t>(ws, L.lb_escan), ctr + 4, at<const uint32_t>(ws, P.total_pairs), L.capacity, ctr + 8,
+        at<uint32_t>(ws, P.overflow));
     if (L.nck_max == 0) return cudaGetLastError();
-    const size_t smem = l1_smem_bytes(L.n_super);
-    cudaError_t e = cudaFuncSetAttribute(k_l1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     const uint32_t *E = ctr + 8;
     int sbits = 1;
     while ((1 << sbits) < L.n_super) ++sbits;
-    k_l1_count<<<L.nck_max, kBinWarps * 32, smem, st>>>(
-        at<const uint32_t>(ws, P.n_visible), E, at<const uint32_t>(ws, P.overflow), at<const uint32_t>(ws, L.wstart),
-        at<const uint32_t>(ws, L.eoff), at<const uint32_t>(ws, P.order), at<const uint4>(ws, P.erec),
-        at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y, L.stx, L.n_super, sbits, at<uint32_t>(ws, L.bin_M),
-        at<uint2>(ws, L.stg));
+    k_entries<<<sms * 8, 256, 0, st>>>(at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, P.overflow),
+                                       at<const uint32_t>(ws, L.eoff), at<const uint32_t>(ws, P.order),
+                                       at<const uint4>(ws, P.erec), at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y,
+                                       L.stx, at<uint2>(ws, L.stg));
+    const size_t smem = l1_smem_bytes(L.n_super);
+    cudaError_t e = cudaFuncSetAttribute(k_l1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_l1_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_l1_count<<<L.nck_max, kBinWarps * 32, smem, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
+                                                        at<const uint2>(ws, L.stg), at<uint32_t>(ws, L.bin_M));
     k_l1_scan<<<L.n_super, 256, 0, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, at<uint32_t>(ws, L.bin_M),
                                          at<uint32_t>(ws, L.st_total), at<uint32_t>(ws, L.st_base),
                                          at<uint32_t>(ws, L.st_blk0), at<uint2>(ws, L.l2_blocks), ctr + 11, ctr + 9);
-    const size_t smem_e = (size_t)kBinWarps * L.n_super * 4;
-    e = cudaFuncSetAttribute(k_l1_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_e);
-    if (e != cudaSuccess) return e;
-    k_l1_emit<<<L.nck_max, kBinWarps * 32, smem_e, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
+    k_l1_emit<<<L.nck_max, kBinWarps * 32, smem, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
                                                          at<const uint32_t>(ws, L.bin_M),
                                                          at<const uint32_t>(ws, L.st_base),
                                                          at<const uint2>(ws, L.stg), at<uint2>(ws, L.ent));

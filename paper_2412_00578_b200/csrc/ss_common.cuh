@@ -27,8 +27,11 @@ constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys per block ti
 constexpr int kInlineEnt = 12;                         // super-tile entries stored in the emission record
 constexpr int kLaneRows = 6;                           // AccuTile lines a preprocess lane sweeps alone
 constexpr int kDepthPasses = 4;                        // 32-bit depth keys, 8-bit digits
-constexpr uint32_t kInfoAccuTile = 0x400u;             // erec info bit: spans follow Algorithm 1
-constexpr int kInfoEntShift = 11;                      // erec info bits 11..31: super-tile entries
+constexpr uint32_t kInfoEntInline = 0x100u;            // erec info: entries stored in the record
+constexpr uint32_t kInfoCols = 0x200u;                 // erec info: columns sweep (lines are tile columns)
+constexpr uint32_t kInfoAccuTile = 0x400u;             // erec info: tile set of Algorithm 1
+constexpr uint32_t kInfoSpanInline = 0x800u;           // erec info: line spans stored in the record
+constexpr int kInfoEntShift = 12;                      // erec info bits 12..31: super-tile entries
 constexpr int kSuperTile = 4;                          // super-tile side in tiles (ss_tilegeom.cuh)
 constexpr int kEntWarp = 256;                          // entries per warp unit of level 1
 constexpr int kBinWarps = 8;                           // warps per level-1 CTA
@@ -47,7 +50,6 @@ struct Layout {
     size_t gne;                     // uint32 [n] super-tile entries per Gaussian (index order)
     size_t one;                     // uint32 [n] the same in depth order
     size_t eoff;                    // uint32 [n] exclusive scan of `one`: first entry of each Gaussian
-    size_t wstart;                  // uint32 [n_units] first Gaussian of each level-1 warp unit
     size_t stg;                     // uint2 [capacity] staged entries (Gaussian, super-tile | mask << 16)
     size_t ent;                     // uint2 [capacity] entries (Gaussian, tile mask) by super-tile
     size_t bin_M;                   // uint32 [nck_max][n_super] entries per (chunk, super-tile) -> prefix
@@ -63,7 +65,7 @@ struct Layout {
     size_t lb_depth;                // uint32 [4][nblk_depth][256]
     size_t lb_escan;                // uint32 [nblk_escan] look-back of the entry scan
     uint32_t nblk_depth, nblk_escan;
-    uint32_t nck_max, n_units;      // level-1 chunks / warp units for `capacity` entries
+    uint32_t nck_max;               // level-1 chunks for `capacity` entries
     uint32_t l2_max_blocks;         // level-2 blocks for `capacity` entries
     int stx, sty, n_super;          // super-tile grid
     int32_t n;

@@ -82,8 +82,12 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
         snug.hx = snug.hy = 0.0;
         uint32_t cols = 0, n_ent = 0;
         bool tall = false;       // AccuTile with more than kLaneRows lines: the warp-collective phase
-        // entries go straight to the emission record (only Gaussians with tiles get one)
+        // entries (or line spans) go straight to the emission record (only Gaussians with tiles
+        // get one; words past the stored count are stale)
         uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 4 * (size_t)i) + 4;
+        uint32_t *span_out = ent_out;
+        uint32_t n_span = 0;
+        bool span_inline = false;
         auto put = [&](uint32_t st, uint32_t mask) {
             if (n_ent < (uint32_t)kInlineEnt) ent_out[n_ent] = st | (mask << 16);
             ++n_ent;
@@ -155,11 +159,18 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
                                                 td, w)) {
                             cols = w.rows ? 0u : 1u;
                             if (w.s1 - w.s0 <= kLaneRows) {
-                                EntryAcc acc;
-                                acc_init(acc, !w.rows, stx);
-                                count = accutile_count(w, cam.tiles_x,
-                                                       [&](int r, int lo, int hi) { acc_feed(acc, r, lo, hi, put); });
-                                acc_flush(acc, put);
+                                // lines stored in the record (level 1 derives the entries from them);
+                                // here only the entry count
+                                EntryCount ec;
+                                cnt_init(ec);
+                                count = accutile_count(w, cam.tiles_x, [&](int r, int lo, int hi) {
+                                    cnt_feed(ec, r, lo, hi);
+                                    if (hi > lo)
+                                        span_out[n_span++] = (uint32_t)lo | ((uint32_t)hi << 9) | ((uint32_t)r << 18);
+                                });
+                                cnt_flush(ec);
+                                n_ent = ec.n;
+                                span_inline = true;
                             } else {
                                 tall = true;
                             }
@@ -265,9 +276,10 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             q[0] = make_float4(x2d, y2d, a, b);
             q[1] = make_float4(c, (float)td, mo.w, 0.0f);
             q[2] = make_float4(0.0f, rgb0, rgb1, rgb2);
-            // emission record (64 B): e0 (count, info, aux0, aux1), e1..e3 = entries 0..11 (written
-            // as they were found; the words past the entry count are stale);
-            // info = inline flag << 8 | columns flag << 9 | AccuTile flag << 10 | entries << 11;
+            // emission record (64 B): e0 (count, info, aux0, aux1), e1..e3 = up to 12 super-tile
+            // entries (super-tile | mask << 16) or, for AccuTile sets of at most kLaneRows lines,
+            // the non-empty line spans (tmin | tmax << 9 | line << 18); info = span count |
+            // entries-inline 0x100 | columns 0x200 | AccuTile 0x400 | spans-inline 0x800 | entries << 12;
             // aux = t as float64 bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1)
             // for the re-enumeration of Gaussians with more than kInlineEnt entries.
             uint32_t aux0, aux1;
@@ -279,8 +291,10 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
                        ((uint32_t)(R.w - R.z - 1) << 24);
                 aux1 = 0u;
             }
-            const uint32_t info = (n_ent <= (uint32_t)kInlineEnt ? 0x100u : 0u) | (cols << 9) |
-                                  (mode == SS_BIN_ACCUTILE ? kInfoAccuTile : 0u) | (n_ent << kInfoEntShift);
+            const uint32_t info = (span_inline ? (kInfoSpanInline | n_span)
+                                               : (n_ent <= (uint32_t)kInlineEnt ? kInfoEntInline : 0u)) |
+                                  (cols ? kInfoCols : 0u) | (mode == SS_BIN_ACCUTILE ? kInfoAccuTile : 0u) |
+                                  (n_ent << kInfoEntShift);
             uint4 *er = erec + 4 * (size_t)i;
             er[0] = make_uint4(count, info, aux0, aux1);
             const uint32_t key = __float_as_uint(pz);

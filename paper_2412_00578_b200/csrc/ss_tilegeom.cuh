@@ -175,9 +175,9 @@ __device__ __forceinline__ uint32_t accutile_count(const Sweep &w, int tiles_x, 
 // (y & 3) * 4 + (x & 3) for tile (x, y)).  Lines of the tile set (tile rows, or tile columns
 // for Algorithm 1's columns sweep) are fed in increasing order with their span [a, b) along
 // the other axis; each band of 4 lines is flushed as entries in increasing order along the
-// span axis.  Masks are never empty: the lines of a band of a convex tile set have
-// overlapping spans (they share the tiles of the band-internal boundary lines), so every
-// super-tile between the band's extremes holds a tile of some line.
+// span axis: one entry for every super-tile between the band's extremes along the span
+// axis (so the count needs only the extremes; for a convex tile set every such mask is
+// non-empty, and an empty one would add no pair).
 constexpr int kSuper = kSuperTile;
 
 struct EntryAcc {
@@ -223,7 +223,7 @@ __device__ __forceinline__ void band_entries(int band, uint32_t iv0, uint32_t iv
     for (int C = lo >> 2; lo < hi && C <= (hi - 1) >> 2; ++C) {
         const uint32_t mask = line_bits(iv0, C, 0, cols) | line_bits(iv1, C, 1, cols) | line_bits(iv2, C, 2, cols) |
                               line_bits(iv3, C, 3, cols);
-        if (mask) emit(cols ? (uint32_t)(C * stx + band) : (uint32_t)(band * stx + C), mask);
+        emit(cols ? (uint32_t)(C * stx + band) : (uint32_t)(band * stx + C), mask);
     }
 }
 
@@ -249,6 +249,34 @@ __device__ __forceinline__ void acc_feed(EntryAcc &A, int line, int a, int b, F 
         case 2: A.iv2 = v; break;
         default: A.iv3 = v; break;
     }
+}
+
+// Entry count of a tile set fed line by line (increasing): per band of 4 lines, the number
+// of super-tiles between the band's extremes.
+struct EntryCount {
+    int band, lo, hi;
+    uint32_t n;
+};
+__device__ __forceinline__ void cnt_init(EntryCount &E) {
+    E.band = -1;
+    E.lo = 1 << 20;
+    E.hi = 0;
+    E.n = 0;
+}
+__device__ __forceinline__ void cnt_flush(EntryCount &E) {
+    if (E.band >= 0 && E.lo < E.hi) E.n += (uint32_t)(((E.hi - 1) >> 2) - (E.lo >> 2) + 1);
+    E.band = -1;
+    E.lo = 1 << 20;
+    E.hi = 0;
+}
+__device__ __forceinline__ void cnt_feed(EntryCount &E, int line, int a, int b) {
+    if (b <= a) return;
+    if ((line >> 2) != E.band) {
+        cnt_flush(E);
+        E.band = line >> 2;
+    }
+    E.lo = min(E.lo, a);
+    E.hi = max(E.hi, b);
 }
 
 // The 4 line spans of band `band` of a prepared AccuTile sweep, evaluated exactly as the
