@@ -80,6 +80,7 @@ __device__ __forceinline__ uint32_t compact_active(bool active, PixState &st, ui
     return n_active;
 }
 
+template <bool NC>  // NC: track the last blended list entry per pixel (out_ncontrib requested)
 __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
                                                 const float4 *__restrict__ rec, int W, int H, int tiles_x, float bg0,
                                                 float bg1, float bg2, float *__restrict__ out_rgb,
@@ -132,13 +133,13 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
                 C1 = fmaf(cl.y, w, C1);
                 C2 = fmaf(cl.z, w, C2);
                 T = Tn;
-                last = contrib ? base + (uint32_t)k : last;
+                if (NC) last = contrib ? base + (uint32_t)k : last;
             }
             st.T[pp] = T;
             st.C0[pp] = C0;
             st.C1[pp] = C1;
             st.C2[pp] = C2;
-            st.last[pp] = last;
+            if (NC) st.last[pp] = last;
             st.done[pp] = done ? 1 : 0;
         }
     }
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
         out_rgb[plane + p] = fmaf(T, bg1, st.C1[p0]);
         out_rgb[2 * plane + p] = fmaf(T, bg2, st.C2[p0]);
         if (out_T) out_T[p] = T;
-        if (out_nc) out_nc[p] = st.last[p0];
+        if (NC) out_nc[p] = st.last[p0];
     }
 }
 
@@ -370,9 +371,14 @@ cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, fl
                           float *out_T, uint32_t *out_nc, cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
-    k_render<<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
-                                         at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb, out_T,
-                                         out_nc);
+    if (out_nc)
+        k_render<true><<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
+                                                   at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
+                                                   out_T, out_nc);
+    else
+        k_render<false><<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
+                                                    at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
+                                                    out_T, out_nc);
     return cudaGetLastError();
 }
 

@@ -206,7 +206,19 @@ __device__ __forceinline__ uint32_t line_bits(uint32_t iv, int C, int q, bool co
     return cols ? (spread4(bits) << q) : (bits << (4 * q));
 }
 
-// Entries of one band given its 4 line spans: emit(super-tile, mask) in increasing order.
+// Transpose of a 4x4 bit matrix stored as 4 nibbles (bit r*4 + c -> bit c*4 + r).
+__device__ __forceinline__ uint32_t transpose4x4(uint32_t w) {
+    uint32_t t = (w ^ (w >> 3)) & 0x0A0Au;
+    w ^= t ^ (t << 3);
+    t = (w ^ (w >> 6)) & 0x00CCu;
+    w ^= t ^ (t << 6);
+    return w;
+}
+
+// Entries of one band given its 4 line spans: emit(super-tile, mask) for every super-tile
+// between the band's extremes along the span axis, in increasing order.  Bands no wider than
+// 32 tiles (from their first super-tile boundary) use 32-bit line bitmaps; wider ones the
+// per-line interval form.  Both give the same masks.
 template <class F>
 __device__ __forceinline__ void band_entries(int band, uint32_t iv0, uint32_t iv1, uint32_t iv2, uint32_t iv3,
                                              bool cols, int stx, F &&emit) {
@@ -220,7 +232,24 @@ __device__ __forceinline__ void band_entries(int band, uint32_t iv0, uint32_t iv
             hi = max(hi, b);
         }
     }
-    for (int C = lo >> 2; lo < hi && C <= (hi - 1) >> 2; ++C) {
+    if (lo >= hi) return;
+    const int ox = lo & ~3;
+    if (hi - ox <= 32) {
+        uint32_t m[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int a = (int)(ivs[q] & 0xFFFFu), b = (int)(ivs[q] >> 16);
+            m[q] = b > a ? (((b - a) >= 32 ? 0xFFFFFFFFu : ((1u << (b - a)) - 1u)) << (a - ox)) : 0u;
+        }
+        for (int C = lo >> 2; C <= (hi - 1) >> 2; ++C) {
+            const int sh = 4 * C - ox;
+            const uint32_t w = ((m[0] >> sh) & 0xFu) | (((m[1] >> sh) & 0xFu) << 4) | (((m[2] >> sh) & 0xFu) << 8) |
+                               (((m[3] >> sh) & 0xFu) << 12);
+            emit(cols ? (uint32_t)(C * stx + band) : (uint32_t)(band * stx + C), cols ? transpose4x4(w) : w);
+        }
+        return;
+    }
+    for (int C = lo >> 2; C <= (hi - 1) >> 2; ++C) {
         const uint32_t mask = line_bits(iv0, C, 0, cols) | line_bits(iv1, C, 1, cols) | line_bits(iv2, C, 2, cols) |
                               line_bits(iv3, C, 3, cols);
         emit(cols ? (uint32_t)(C * stx + band) : (uint32_t)(band * stx + C), mask);

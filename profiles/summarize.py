@@ -6,6 +6,7 @@
 import collections
 import csv
 import io
+import os
 import subprocess
 import sys
 
@@ -68,8 +69,10 @@ def traffic(*paths):
             b = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
             us = float(r[it]) * (1e-3 if units[it] == "nsecond" else 1.0)
             agg[name].append((b, us))
-    print(json.dumps({k: {"dram_bytes": sum(b for b, _ in v) / len(v), "us": sum(u for _, u in v) / len(v),
-                          "captures": len(v)} for k, v in agg.items()}, indent=1))
+    src = ", ".join(os.path.basename(p) for p in paths)
+    print(json.dumps({"source": f"ncu --set full ({src}): dram__bytes_read.sum + dram__bytes_write.sum per launch",
+                      "kernels": {k: {"dram_bytes": sum(b for b, _ in v) / len(v), "us": sum(u for _, u in v) / len(v),
+                                      "captures": len(v)} for k, v in agg.items()}}, indent=1))
 
 
 if __name__ == "__main__":
