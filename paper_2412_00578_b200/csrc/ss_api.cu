@@ -48,6 +48,7 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     L->gne = take(4 * N);
     L->one = take(4 * N);
     L->eoff = take(4 * N);
+    L->big_queue = take(4 * N);
     L->stg = take(8 * Cap);
     L->ent = take(8 * Cap);
     L->bin_M = take(4 * S * (size_t)L->nck_max);

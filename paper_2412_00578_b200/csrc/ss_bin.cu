@@ -225,13 +225,15 @@ __device__ __noinline__ void big_entries(uint2 *__restrict__ stg, uint32_t g, ui
 }
 
 // Every visible Gaussian's entries, in depth order, written to their global entry slots
-// stg[eoff[k] ..] (one thread per Gaussian; Gaussians with more than kInlineEnt entries by
-// the whole warp).  Warp-uniform grid-stride loop.
+// stg[eoff[k] ..] (one thread per Gaussian; Gaussians with more than kInlineEnt entries are
+// queued for k_big_entries).  Warp-uniform grid-stride loop.
 __global__ void __launch_bounds__(256) k_entries(const uint32_t *__restrict__ n_visible,
                                                  const uint32_t *__restrict__ overflow,
                                                  const uint32_t *__restrict__ eoff, const uint32_t *__restrict__ order,
                                                  const uint4 *__restrict__ erec, const float4 *__restrict__ rec,
-                                                 int tiles_x, int tiles_y, int stx, uint2 *__restrict__ stg) {
+                                                 int tiles_x, int tiles_y, int stx, uint2 *__restrict__ stg,
+                                                 uint32_t *__restrict__ big_count,
+                                                 uint32_t *__restrict__ big_queue) {
     if (*overflow) return;
     const uint32_t nv = *n_visible;
     const int lane = threadIdx.x & 31;
@@ -255,14 +257,35 @@ __global__ void __launch_bounds__(256) k_entries(const uint32_t *__restrict__ n_
         const bool spn = (e0.y & kInfoSpanInline) != 0, ent = (e0.y & kInfoEntInline) != 0;
         if (act && spn) span_entries(stg, g, eo, e0.y, e1, e2, stx);
         if (act && ent) inline_entries(stg, g, eo, e0.y >> kInfoEntShift, e1, e2, e3);
-        uint32_t big = __ballot_sync(0xffffffffu, act && !spn && !ent);
-        while (big) {
-            const int src = __ffs(big) - 1;
-            big &= big - 1;
-            big_entries(stg, __shfl_sync(0xffffffffu, g, src), __shfl_sync(0xffffffffu, eo, src),
-                        __shfl_sync(0xffffffffu, e0.y, src), __shfl_sync(0xffffffffu, e0.z, src),
-                        __shfl_sync(0xffffffffu, e0.w, src), rec, tiles_x, tiles_y, stx);
+        // Gaussians with more entries than inline slots (a few hundred, the nearest ones, so
+        // clustered at the front of the depth order): queued for k_big_entries, a warp each
+        const bool big = act && !spn && !ent;
+        const uint32_t bmask = __ballot_sync(0xffffffffu, big);
+        if (bmask) {
+            uint32_t base = 0;
+            if (lane == __ffs(bmask) - 1) base = atomicAdd(big_count, (uint32_t)__popc(bmask));
+            base = __shfl_sync(0xffffffffu, base, __ffs(bmask) - 1);
+            if (big) big_queue[base + __popc(bmask & ((1u << lane) - 1u))] = k;
         }
+    }
+}
+
+// The queued Gaussians' entries, one warp per Gaussian (warp-uniform loop).
+__global__ void __launch_bounds__(256) k_big_entries(const uint32_t *__restrict__ overflow,
+                                                     const uint32_t *__restrict__ big_count,
+                                                     const uint32_t *__restrict__ big_queue,
+                                                     const uint32_t *__restrict__ eoff,
+                                                     const uint32_t *__restrict__ order,
+                                                     const uint4 *__restrict__ erec, const float4 *__restrict__ rec,
+                                                     int tiles_x, int tiles_y, int stx, uint2 *__restrict__ stg) {
+    if (*overflow) return;
+    const uint32_t nb = *big_count;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nb; q += warps) {
+        const uint32_t k = big_queue[q];
+        const uint32_t g = order[k];
+        const uint4 e0 = erec[4 * (size_t)g];
+        big_entries(stg, g, eoff[k], e0.y, e0.z, e0.w, rec, tiles_x, tiles_y, stx);
     }
 }
 
@@ -658,7 +681,12 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
     k_entries<<<sms * 8, 256, 0, st>>>(at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, P.overflow),
                                        at<const uint32_t>(ws, L.eoff), at<const uint32_t>(ws, P.order),
                                        at<const uint4>(ws, P.erec), at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y,
-                                       L.stx, at<uint2>(ws, L.stg));
+                                       L.stx, at<uint2>(ws, L.stg), ctr + 12, at<uint32_t>(ws, L.big_queue));
+    k_big_entries<<<sms * 4, 256, 0, st>>>(at<const uint32_t>(ws, P.overflow), ctr + 12,
+                                           at<const uint32_t>(ws, L.big_queue), at<const uint32_t>(ws, L.eoff),
+                                           at<const uint32_t>(ws, P.order), at<const uint4>(ws, P.erec),
+                                           at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y, L.stx,
+                                           at<uint2>(ws, L.stg));
     const size_t smem = l1_smem_bytes(L.n_super);
     cudaError_t e = cudaFuncSetAttribute(k_l1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_l1_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -50,6 +50,7 @@ struct Layout {
     size_t gne;                     // uint32 [n] super-tile entries per Gaussian (index order)
     size_t one;                     // uint32 [n] the same in depth order
     size_t eoff;                    // uint32 [n] exclusive scan of `one`: first entry of each Gaussian
+    size_t big_queue;               // uint32 [n] depth positions of Gaussians with non-inline entries
     size_t stg;                     // uint2 [capacity] staged entries (Gaussian, super-tile | mask << 16)
     size_t ent;                     // uint2 [capacity] entries (Gaussian, tile mask) by super-tile
     size_t bin_M;                   // uint32 [nck_max][n_super] entries per (chunk, super-tile) -> prefix
