@@ -66,15 +66,17 @@ typedef enum {
 
 /* Gaussian set G = {mu, s, r, h, sigma} (Eq. 1), SoA float32 planes in HBM.
  * Parameters are ACTIVATED: linear scales, opacity in (0,1); the quaternion is normalised
- * in-kernel.  SH coefficient k = basis*3 + channel is component k%4 of plane k/4; plane p
- * is the float4 array sh + 4*n*p.  Planes: deg 0 -> 1, 1 -> 3, 2 -> 7, 3 -> 12. */
+ * in-kernel.  SH coefficient k = basis*3 + channel of Gaussian i is component k%4 of float4
+ * sh[i*B + k/4]: one contiguous block of B float4 per Gaussian (B = 1, 3, 7, 12 for degree
+ * 0..3), so that the 16*B bytes of a Gaussian with tiles are read whole and those of the
+ * others not at all. */
 typedef struct {
     int32_t n;              /* number of Gaussians, 0 <= n < 2^30                            */
     int32_t sh_degree;      /* 0..3                                                          */
     const float *mean_opac; /* [n][4]  x, y, z (world), opacity sigma                         */
     const float *scale;     /* [n][4]  sx, sy, sz (linear), unused                            */
     const float *rot;       /* [n][4]  quaternion w, x, y, z                                  */
-    const float *sh;        /* [planes][n][4]                                                 */
+    const float *sh;        /* [n][B][4] per-Gaussian SH blocks                                */
 } ss_scene;
 
 /* Pinhole camera (host struct, copied into kernel arguments).  Pixel (col,row) has
@@ -190,9 +192,9 @@ SS_API ss_status ss_prune_score(const ss_frame *frame /*host*/, const float *bg 
  * ss_prune_select: keep[i] (device uint8 [n]) = 0 for exactly k = ss_prune_count(n, ratio) =
  * floor(ratio n) Gaussians with the smallest score (device float64 [n], e.g. the all-reduced
  * U~); on equal scores the higher index is removed first.  ratio in [0, 1].
- * ss_compact_scene: stable stream compaction of every SoA plane of `in` into `out` (device
- * planes allocated by the caller for out->n = n - k Gaussians; out->sh planes have stride
- * out->n); *n_out (device uint32) receives the survivor count.  Both use a caller workspace
+ * ss_compact_scene: stable stream compaction of every array of `in` into `out` (device arrays
+ * allocated by the caller for out->n = n - k Gaussians); *n_out (device uint32) receives the
+ * survivor count.  Both use a caller workspace
  * of ss_prune_workspace_size(n) bytes (device). */
 SS_API size_t ss_prune_workspace_size(int32_t n);
 SS_API uint32_t ss_prune_count(int32_t n, double ratio);

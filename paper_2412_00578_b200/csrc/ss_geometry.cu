@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             float hc[NP * 4];
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
-                const float4 v = __ldg(sh + (size_t)p * n + i);
+                const float4 v = __ldg(sh + (size_t)i * NP + p);  // the Gaussian's contiguous SH block
                 hc[4 * p + 0] = v.x;
                 hc[4 * p + 1] = v.y;
                 hc[4 * p + 2] = v.z;

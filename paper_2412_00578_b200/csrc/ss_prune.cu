@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(256) k_compact(int n, const uint8_t *__restric
             mo_out[o] = mo_in[i];
             sc_out[o] = sc_in[i];
             rot_out[o] = rot_in[i];
-            for (int p = 0; p < n_planes_sh; ++p) sh_out[(size_t)p * out_stride + o] = sh_in[(size_t)p * n + i];
+            for (int p = 0; p < n_planes_sh; ++p)  // per-Gaussian SH block (AoS)
+                sh_out[(size_t)o * n_planes_sh + p] = sh_in[(size_t)i * n_planes_sh + p];
         }
     }
 }

@@ -30,6 +30,7 @@ struct Snug {
     double xmin, xmax, ymin, ymax;
     double yl, yr;   // y of the x_min / x_max tangent points (B_l, B_r)
     double xt, xb;   // x of the y_min / y_max tangent points (B_t, B_b)
+    double ia, ic;   // 1 / a, 1 / c
 };
 
 __device__ __forceinline__ Snug snugbox(double mx, double my, double a, double b, double c, double t) {
@@ -50,6 +51,8 @@ __device__ __forceinline__ Snug snugbox(double mx, double my, double a, double b
     s.yr = my - b * hx * ic;
     s.xt = mx + b * hy * ia;
     s.xb = mx - b * hy * ia;
+    s.ia = ia;
+    s.ic = ic;
     return s;
 }
 
@@ -76,13 +79,13 @@ __device__ __forceinline__ int4 rect_3sigma(double mx, double my, double cxx, do
 }
 
 // Eq. 15 on a line of the swept axis: u = (-b v +- sqrt((b^2 - a_f c_s) v^2 + t a_f)) / a_f.
-__device__ __forceinline__ void intersect_line(double m_free, double m_line, double a_free, double b, double c_line,
-                                               double t, double line, double &lo, double &hi) {
+// ia = 1 / a_free (one reciprocal per Gaussian, R1).
+__device__ __forceinline__ void intersect_line(double m_free, double m_line, double a_free, double ia, double b,
+                                               double c_line, double t, double line, double &lo, double &hi) {
     double v = line - m_line;
     double disc = (b * b - a_free * c_line) * v * v + t * a_free;
     if (disc < 0.0) disc = 0.0;  // R12
     double s = sqrt(disc);
-    double ia = 1.0 / a_free;
     lo = m_free + (-b * v - s) * ia;
     hi = m_free + (-b * v + s) * ia;
 }
@@ -93,6 +96,7 @@ __device__ __forceinline__ void intersect_line(double m_free, double m_line, dou
 struct Sweep {
     bool rows;                                        // rows path (else columns)
     double mf, ms, af, cs, b, t;                      // free/swept-axis centre and coefficients
+    double iaf;                                       // 1 / af
     double ext_lo, ext_hi, smin, smax, tmin_s, tmax_s;
     int s0, s1, f0, f1;                               // swept lines [s0, s1), free span [f0, f1)
 };
@@ -104,12 +108,12 @@ __device__ __forceinline__ bool accutile_setup_from(const Snug &S, const int4 &R
     w.b = b;
     w.t = t;
     if (w.rows) {
-        w.mf = mx; w.ms = my; w.af = a; w.cs = c;
+        w.mf = mx; w.ms = my; w.af = a; w.cs = c; w.iaf = S.ia;
         w.ext_lo = S.xmin; w.ext_hi = S.xmax; w.smin = S.ymin; w.smax = S.ymax;
         w.tmin_s = S.yl; w.tmax_s = S.yr;
         w.s0 = R.z; w.s1 = R.w; w.f0 = R.x; w.f1 = R.y;
     } else {
-        w.mf = my; w.ms = mx; w.af = c; w.cs = a;
+        w.mf = my; w.ms = mx; w.af = c; w.cs = a; w.iaf = S.ic;
         w.ext_lo = S.ymin; w.ext_hi = S.ymax; w.smin = S.xmin; w.smax = S.xmax;
         w.tmin_s = S.xt; w.tmax_s = S.xb;
         w.s0 = R.x; w.s1 = R.y; w.f0 = R.z; w.f1 = R.w;
@@ -128,7 +132,7 @@ __device__ __forceinline__ bool accutile_setup(double mx, double my, double a, d
 __device__ __forceinline__ void sweep_line(const Sweep &w, double line, bool compute, double &lo, double &hi) {
     lo = __longlong_as_double(0x7ff0000000000000ll);   // +inf
     hi = __longlong_as_double(0xfff0000000000000ll);   // -inf
-    if (compute) intersect_line(w.mf, w.ms, w.af, w.b, w.cs, w.t, line, lo, hi);
+    if (compute) intersect_line(w.mf, w.ms, w.af, w.iaf, w.b, w.cs, w.t, line, lo, hi);
 }
 
 // One row (or column) r of Algorithm 1 given i_min (its lower boundary line) and i_max (its

@@ -27,7 +27,7 @@ class DeviceScene:
     mean_opac: torch.Tensor   # [N,4] f32 cuda
     scale: torch.Tensor       # [N,4]
     rot: torch.Tensor         # [N,4]
-    sh: torch.Tensor          # [P,N,4]
+    sh: torch.Tensor          # [N,B,4] per-Gaussian SH blocks
     sh_degree: int
 
     @property
@@ -37,7 +37,9 @@ class DeviceScene:
     @staticmethod
     def from_host(scene, device="cuda") -> "DeviceScene":
         t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(device)
-        return DeviceScene(t(scene.mean_opac), t(scene.scale), t(scene.rot), t(scene.sh), int(scene.sh_degree))
+        # SH: host planes [B][N][4] -> the device's per-Gaussian blocks [N][B][4] (include/ss.h)
+        return DeviceScene(t(scene.mean_opac), t(scene.scale), t(scene.rot), t(np.transpose(scene.sh, (1, 0, 2))),
+                           int(scene.sh_degree))
 
     def struct(self) -> SsScene:
         return SsScene(self.n, self.sh_degree, self.mean_opac.data_ptr(), self.scale.data_ptr(),
@@ -247,7 +249,7 @@ def prune(scene: DeviceScene, score: torch.Tensor, ratio: float, stream=None) ->
     out = DeviceScene(torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
                       torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
                       torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
-                      torch.empty((scene.sh.shape[0], m, 4), dtype=torch.float32, device=dev), scene.sh_degree)
+                      torch.empty((m, scene.sh.shape[1], 4), dtype=torch.float32, device=dev), scene.sh_degree)
     n_out = torch.zeros(1, dtype=torch.int32, device=dev)
     src, dst = scene.struct(), out.struct()
     check(lib().ss_compact_scene(C.byref(src), C.c_void_p(keep.data_ptr()), C.byref(dst),

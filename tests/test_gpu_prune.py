@@ -27,7 +27,7 @@ def test_prune_select_and_compact(ratio):
     assert np.array_equal(out.mean_opac.cpu().numpy(), scene.mean_opac[idx])
     assert np.array_equal(out.rot.cpu().numpy(), scene.rot[idx])
     assert np.array_equal(out.scale.cpu().numpy(), scene.scale[idx])
-    assert np.array_equal(out.sh.cpu().numpy(), scene.sh[:, idx])
+    assert np.array_equal(out.sh.cpu().numpy(), np.transpose(scene.sh[:, idx], (1, 0, 2)))
 
 
 def test_score_then_prune_renders():
