@@ -16,7 +16,8 @@
  *
  * Conventions (DESIGN.md §2-§3 states every reading of the paper behind them):
  *   - Every pointer is a DEVICE pointer unless marked (host).  Device buffers are owned by
- *     the caller; libss never allocates, frees or keeps global state.  All calls enqueue
+ *     the caller; libss never allocates or frees device memory and keeps no per-frame state
+ *     (it caches the device's SM count and raises kernels' shared-memory limits once).  All calls enqueue
  *     work on `stream` (a cudaStream_t passed as void*, NULL = legacy default stream) and
  *     return without synchronising.  Calls on different streams with disjoint frame
  *     workspaces may run concurrently.

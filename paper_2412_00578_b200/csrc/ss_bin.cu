@@ -666,9 +666,7 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
         return e;
     }
     uint32_t *ctr = at<uint32_t>(ws, L.counters);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     const int scan_grid = (int)L.nblk_escan < sms * 4 ? (int)L.nblk_escan : sms * 4;
     k_entry_scan<<<scan_grid > 0 ? scan_grid : 1, kScanThreads, 0, st>>>(
         at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, L.one), at<uint32_t>(ws, L.eoff),
@@ -688,8 +686,9 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
                                            at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y, L.stx,
                                            at<uint2>(ws, L.stg));
     const size_t smem = l1_smem_bytes(L.n_super);
-    cudaError_t e = cudaFuncSetAttribute(k_l1_count, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_l1_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static int smem_count[64] = {0}, smem_emit[64] = {0};
+    cudaError_t e = ensure_smem(k_l1_count, smem, smem_count);
+    if (e == cudaSuccess) e = ensure_smem(k_l1_emit, smem, smem_emit);
     if (e != cudaSuccess) return e;
     k_l1_count<<<L.nck_max, kBinWarps * 32, smem, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
                                                         at<const uint2>(ws, L.stg), at<uint32_t>(ws, L.bin_M));

@@ -80,6 +80,33 @@ __host__ __device__ inline T *at(void *ws, size_t off) {
     return reinterpret_cast<T *>(static_cast<char *>(ws) + off);
 }
 
+// Streaming-multiprocessor count of the current device, queried once per device and cached
+// (launch-configuration data only: the frame path stays free of host-side device queries).
+inline int sm_count() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (cache[dev] == 0) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = sms > 0 ? sms : 148;
+    }
+    return cache[dev];
+}
+
+// Raises a kernel's dynamic shared-memory limit to `bytes` once per device (idempotent).
+template <class K>
+inline cudaError_t ensure_smem(K kernel, size_t bytes, int *done /* [64] per device */) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (done[dev] >= (int)bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done[dev] = (int)bytes;
+    return e;
+}
+
 // Launchers implemented in the kernel translation units.
 cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, void *ws, const Layout &L,
                               cudaStream_t st);

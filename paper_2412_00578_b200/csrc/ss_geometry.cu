@@ -336,9 +336,7 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
                               cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (sc.n == 0) return cudaSuccess;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     const int blocks_needed = (sc.n + 255) / 256;
     const int grid = blocks_needed < sms * 8 ? blocks_needed : sms * 8;
 #define SS_PRE_ARGS                                                                                       \

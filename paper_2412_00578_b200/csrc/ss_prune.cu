@@ -179,9 +179,7 @@ __global__ void __launch_bounds__(256) k_compact(int n, const uint8_t *__restric
 }
 
 int grid_for(int n) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     const int need = (n + 255) / 256;
     return need < sms * 4 ? (need > 0 ? need : 1) : sms * 4;
 }

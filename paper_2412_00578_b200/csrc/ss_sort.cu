@@ -186,9 +186,7 @@ __global__ void k_sorted_keys(const uint2 *__restrict__ ranges, const uint32_t *
 }
 
 int sort_grid(uint32_t nblk) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = sm_count();
     const uint32_t cap = (uint32_t)sms * 4;
     return (int)(nblk < cap ? (nblk ? nblk : 1) : cap);
 }
