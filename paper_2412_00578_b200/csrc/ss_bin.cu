@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kScanThreads) k_entry_scan(const uint32_t *__r
                                                              const uint32_t *__restrict__ total_pairs, uint32_t cap,
                                                              uint32_t *__restrict__ total_entries,
                                                              uint32_t *__restrict__ overflow) {
+    pdl_enter();
     __shared__ uint32_t s_warp[8];
     __shared__ uint32_t s_bid, s_base;
     const uint32_t nv = *n_visible;
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(256) k_entries(const uint32_t *__restrict__ n_
                                                  int tiles_x, int tiles_y, int stx, uint2 *__restrict__ stg,
                                                  uint32_t *__restrict__ big_count,
                                                  uint32_t *__restrict__ big_queue) {
+    pdl_enter();
     if (*overflow) return;
     const uint32_t nv = *n_visible;
     const int lane = threadIdx.x & 31;
@@ -278,6 +280,7 @@ __global__ void __launch_bounds__(256) k_big_entries(const uint32_t *__restrict_
                                                      const uint32_t *__restrict__ order,
                                                      const uint4 *__restrict__ erec, const float4 *__restrict__ rec,
                                                      int tiles_x, int tiles_y, int stx, uint2 *__restrict__ stg) {
+    pdl_enter();
     if (*overflow) return;
     const uint32_t nb = *big_count;
     const uint32_t warps = gridDim.x * (blockDim.x >> 5);
@@ -311,6 +314,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_l1_count(const uint32_t *__r
                                                               const uint32_t *__restrict__ overflow, int n_super,
                                                               int sbits, const uint2 *__restrict__ stg,
                                                               uint32_t *__restrict__ M) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw);
     const uint32_t E = *total_entries, c = blockIdx.x;
@@ -356,6 +360,7 @@ __global__ void __launch_bounds__(256) k_l1_scan(const uint32_t *__restrict__ to
                                                  uint32_t *__restrict__ st_base, uint32_t *__restrict__ st_blk0,
                                                  uint2 *__restrict__ blocks, uint32_t *__restrict__ n_blocks,
                                                  uint32_t *done) {
+    pdl_enter();
     __shared__ uint32_t s_warp[8];
     __shared__ bool s_last;
     if (*overflow) return;
@@ -419,6 +424,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_l1_emit(const uint32_t *__re
                                                              int sbits, const uint32_t *__restrict__ M,
                                                              const uint32_t *__restrict__ st_base,
                                                              const uint2 *__restrict__ stg, uint2 *__restrict__ ent) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw);
     const uint32_t E = *total_entries, c = blockIdx.x;
@@ -503,6 +509,7 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_count(const uint32_t *__restr
                                                          const uint2 *__restrict__ blocks,
                                                          const uint32_t *__restrict__ n_blocks,
                                                          const uint2 *__restrict__ ent, uint32_t *__restrict__ BC) {
+    pdl_enter();
     __shared__ uint32_t s_cnt[kL2Threads / 32][16];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const bool ovf = *overflow != 0;
@@ -540,6 +547,7 @@ __global__ void __launch_bounds__(1024) k_l2_scan(const uint32_t *__restrict__ o
                                                   const uint32_t *__restrict__ st_blk0, uint32_t *__restrict__ BC,
                                                   uint32_t *__restrict__ tile_count, uint32_t *__restrict__ tile_base,
                                                   uint2 *__restrict__ ranges) {
+    pdl_enter();
     __shared__ uint32_t s_warp[32];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const bool ovf = *overflow != 0;
@@ -608,6 +616,7 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_write(const uint32_t *__restr
                                                          const uint32_t *__restrict__ BC,
                                                          const uint32_t *__restrict__ tile_base,
                                                          uint32_t *__restrict__ sorted_value) {
+    pdl_enter();
     __shared__ uint32_t s_bal[kL2Threads / 32][16];
     __shared__ uint32_t s_off[kL2Threads / 32][16];
     __shared__ uint32_t s_run[16];
@@ -668,7 +677,7 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
     uint32_t *ctr = at<uint32_t>(ws, L.counters);
     const int sms = sm_count();
     const int scan_grid = (int)L.nblk_escan < sms * 4 ? (int)L.nblk_escan : sms * 4;
-    k_entry_scan<<<scan_grid > 0 ? scan_grid : 1, kScanThreads, 0, st>>>(
+    launch_pdl(k_entry_scan, scan_grid > 0 ? scan_grid : 1, kScanThreads, 0, st, 
         at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, L.one), at<uint32_t>(ws, L.eoff),
         at<uint32_t>(ws, L.lb_escan), ctr + 4, at<const uint32_t>(ws, P.total_pairs), L.capacity, ctr + 8,
         at<uint32_t>(ws, P.overflow));
@@ -676,11 +685,11 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
     const uint32_t *E = ctr + 8;
     int sbits = 1;
     while ((1 << sbits) < L.n_super) ++sbits;
-    k_entries<<<sms * 8, 256, 0, st>>>(at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, P.overflow),
+    launch_pdl(k_entries, sms * 8, 256, 0, st, at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, P.overflow),
                                        at<const uint32_t>(ws, L.eoff), at<const uint32_t>(ws, P.order),
                                        at<const uint4>(ws, P.erec), at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y,
                                        L.stx, at<uint2>(ws, L.stg), ctr + 12, at<uint32_t>(ws, L.big_queue));
-    k_big_entries<<<sms * 4, 256, 0, st>>>(at<const uint32_t>(ws, P.overflow), ctr + 12,
+    launch_pdl(k_big_entries, sms * 4, 256, 0, st, at<const uint32_t>(ws, P.overflow), ctr + 12,
                                            at<const uint32_t>(ws, L.big_queue), at<const uint32_t>(ws, L.eoff),
                                            at<const uint32_t>(ws, P.order), at<const uint4>(ws, P.erec),
                                            at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y, L.stx,
@@ -690,20 +699,20 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
     cudaError_t e = ensure_smem(k_l1_count, smem, smem_count);
     if (e == cudaSuccess) e = ensure_smem(k_l1_emit, smem, smem_emit);
     if (e != cudaSuccess) return e;
-    k_l1_count<<<L.nck_max, kBinWarps * 32, smem, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
+    launch_pdl(k_l1_count, L.nck_max, kBinWarps * 32, smem, st, E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
                                                         at<const uint2>(ws, L.stg), at<uint32_t>(ws, L.bin_M));
-    k_l1_scan<<<L.n_super, 256, 0, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, at<uint32_t>(ws, L.bin_M),
+    launch_pdl(k_l1_scan, L.n_super, 256, 0, st, E, at<const uint32_t>(ws, P.overflow), L.n_super, at<uint32_t>(ws, L.bin_M),
                                          at<uint32_t>(ws, L.st_total), at<uint32_t>(ws, L.st_base),
                                          at<uint32_t>(ws, L.st_blk0), at<uint2>(ws, L.l2_blocks), ctr + 11, ctr + 9);
-    k_l1_emit<<<L.nck_max, kBinWarps * 32, smem, st>>>(E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
+    launch_pdl(k_l1_emit, L.nck_max, kBinWarps * 32, smem, st, E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
                                                          at<const uint32_t>(ws, L.bin_M),
                                                          at<const uint32_t>(ws, L.st_base),
                                                          at<const uint2>(ws, L.stg), at<uint2>(ws, L.ent));
-    k_l2_count<<<L.l2_max_blocks, kL2Threads, 0, st>>>(
+    launch_pdl(k_l2_count, L.l2_max_blocks, kL2Threads, 0, st, 
         at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super, at<const uint32_t>(ws, L.st_total),
         at<const uint32_t>(ws, L.st_base), at<const uint32_t>(ws, L.st_blk0), at<const uint2>(ws, L.l2_blocks),
         ctr + 11, at<const uint2>(ws, L.ent), at<uint32_t>(ws, L.l2_BC));
-    k_l2_scan<<<1, 1024, 0, st>>>(at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super,
+    launch_pdl(k_l2_scan, 1, 1024, 0, st, at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super,
                                   at<const uint32_t>(ws, L.st_total), at<const uint32_t>(ws, L.st_blk0),
                                   at<uint32_t>(ws, L.l2_BC), at<uint32_t>(ws, P.tile_count),
                                   at<uint32_t>(ws, L.tile_base), at<uint2>(ws, P.ranges));
@@ -714,7 +723,7 @@ cudaError_t launch_tile_write(void *ws, const Layout &L, cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0 || L.n == 0 || L.capacity == 0) return cudaSuccess;
     uint32_t *ctr = at<uint32_t>(ws, L.counters);
-    k_l2_write<<<L.l2_max_blocks, kL2Threads, 0, st>>>(
+    launch_pdl(k_l2_write, L.l2_max_blocks, kL2Threads, 0, st, 
         at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, at<const uint32_t>(ws, L.st_total),
         at<const uint32_t>(ws, L.st_base), at<const uint2>(ws, L.l2_blocks), ctr + 11, at<const uint2>(ws, L.ent),
         at<const uint32_t>(ws, L.l2_BC), at<const uint32_t>(ws, L.tile_base), at<uint32_t>(ws, P.sorted_value));

@@ -1,6 +1,7 @@
 // ss_common.cuh -- shared device/host definitions of libss (CUDA path only).
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "../../include/ss.h"
@@ -105,6 +106,31 @@ inline cudaError_t ensure_smem(K kernel, size_t bytes, int *done /* [64] per dev
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e == cudaSuccess) done[dev] = (int)bytes;
     return e;
+}
+
+// Programmatic dependent launch: a frame-path kernel may be launched while its predecessor
+// in the stream drains; it waits (griddepcontrol.wait) for the predecessor's completion and
+// memory before touching anything, then lets its own successor launch.  On a plain launch
+// both instructions are no-ops.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // Launchers implemented in the kernel translation units.

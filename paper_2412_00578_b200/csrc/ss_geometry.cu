@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
                                                     uint32_t *__restrict__ hist,
                                                     uint32_t *__restrict__ n_visible,
                                                     uint32_t *__restrict__ total_pairs) {
+    pdl_enter();
     __shared__ uint32_t s_hist[kDepthPasses][256];
     __shared__ uint32_t s_vis, s_pairs;
     for (int k = threadIdx.x; k < kDepthPasses * 256; k += blockDim.x) (&s_hist[0][0])[k] = 0;
@@ -345,10 +346,10 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
         at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key), at<uint32_t>(ws, L.gne), \
         at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs)
     switch (sc.sh_degree) {
-        case 0: k_preprocess<0><<<grid, 256, 0, st>>>(SS_PRE_ARGS); break;
-        case 1: k_preprocess<1><<<grid, 256, 0, st>>>(SS_PRE_ARGS); break;
-        case 2: k_preprocess<2><<<grid, 256, 0, st>>>(SS_PRE_ARGS); break;
-        default: k_preprocess<3><<<grid, 256, 0, st>>>(SS_PRE_ARGS); break;
+        case 0: launch_pdl(k_preprocess<0>, grid, 256, 0, st, SS_PRE_ARGS); break;
+        case 1: launch_pdl(k_preprocess<1>, grid, 256, 0, st, SS_PRE_ARGS); break;
+        case 2: launch_pdl(k_preprocess<2>, grid, 256, 0, st, SS_PRE_ARGS); break;
+        default: launch_pdl(k_preprocess<3>, grid, 256, 0, st, SS_PRE_ARGS); break;
     }
 #undef SS_PRE_ARGS
     return cudaGetLastError();

@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
                                                 const float4 *__restrict__ rec, int W, int H, int tiles_x, float bg0,
                                                 float bg1, float bg2, float *__restrict__ out_rgb,
                                                 float *__restrict__ out_T, uint32_t *__restrict__ out_nc) {
+    pdl_enter();
     __shared__ Batch s;
     __shared__ PixState st;
     __shared__ uint32_t s_warp[8];
@@ -167,6 +168,7 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
                                                      const uint32_t *__restrict__ vals,
                                                      const float4 *__restrict__ rec, int W, int H, int tiles_x,
                                                      float bg0, float bg1, float bg2, double *__restrict__ score) {
+    pdl_enter();
     __shared__ Batch s;
     __shared__ PixState st;  // forward: T, last, done; backward: T (running), C0..2 = suffix S
     __shared__ float s_Tfin[256];
@@ -372,11 +374,11 @@ cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, fl
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
     if (out_nc)
-        k_render<true><<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
+        launch_pdl(k_render<true>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
                                                    at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
                                                    out_T, out_nc);
     else
-        k_render<false><<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
+        launch_pdl(k_render<false>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
                                                     at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
                                                     out_T, out_nc);
     return cudaGetLastError();
@@ -386,7 +388,7 @@ cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg
                                double *score, cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
-    k_prune_score<<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
+    launch_pdl(k_prune_score, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
                                               at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, score);
     return cudaGetLastError();
 }

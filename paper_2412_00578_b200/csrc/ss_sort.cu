@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restric
                                                               uint32_t *lookback, uint32_t *ticket,
                                                               const uint32_t *__restrict__ gather_src = nullptr,
                                                               uint32_t *__restrict__ gather_dst = nullptr) {
+    pdl_enter();
     __shared__ uint32_t s_whist[kWarps][256];
     __shared__ uint32_t s_digit_base[256];
     __shared__ uint32_t s_dig_out[256];
@@ -204,13 +205,14 @@ cudaError_t launch_depth_sort(void *ws, const Layout &L, cudaStream_t st) {
     const uint32_t *nvis = at<uint32_t>(ws, P.n_visible);
     uint32_t *kA = at<uint32_t>(ws, L.dkA), *vA = at<uint32_t>(ws, L.dvA);
     uint32_t *kB = at<uint32_t>(ws, L.dkB), *vB = at<uint32_t>(ws, L.dvB);
-    k_onesweep<uint32_t, true, true, true><<<grid, kSortThreads, 0, st>>>(
-        at<uint32_t>(ws, P.depth_key), nullptr, kA, vA, nullptr, (uint32_t)L.n, 0, hist, lb, tick + 0);
-    k_onesweep<uint32_t, false, false, true><<<grid, kSortThreads, 0, st>>>(kA, vA, kB, vB, nvis, 0, 8, hist + 256,
-                                                                          lb + lbs, tick + 1);
-    k_onesweep<uint32_t, false, false, true><<<grid, kSortThreads, 0, st>>>(kB, vB, kA, vA, nvis, 0, 16, hist + 512,
-                                                                          lb + 2 * lbs, tick + 2);
-    k_onesweep<uint32_t, false, false, false><<<grid, kSortThreads, 0, st>>>(
+    launch_pdl(k_onesweep<uint32_t, true, true, true>, grid, kSortThreads, 0, st, 
+        at<uint32_t>(ws, P.depth_key), nullptr, kA, vA, nullptr, (uint32_t)L.n, 0, hist, lb, tick + 0, nullptr,
+        nullptr);
+    launch_pdl(k_onesweep<uint32_t, false, false, true>, grid, kSortThreads, 0, st, kA, vA, kB, vB, nvis, 0, 8, hist + 256,
+               lb + lbs, tick + 1, nullptr, nullptr);
+    launch_pdl(k_onesweep<uint32_t, false, false, true>, grid, kSortThreads, 0, st, kB, vB, kA, vA, nvis, 0, 16, hist + 512,
+               lb + 2 * lbs, tick + 2, nullptr, nullptr);
+    launch_pdl(k_onesweep<uint32_t, false, false, false>, grid, kSortThreads, 0, st, 
         kA, vA, nullptr, at<uint32_t>(ws, P.order), nvis, 0, 24, hist + 768, lb + 3 * lbs, tick + 3,
         at<const uint32_t>(ws, L.gne), at<uint32_t>(ws, L.one));
     return cudaGetLastError();
