@@ -402,9 +402,9 @@ def run_ours(args):
             "render_work": {"E_pix": mean(E_pix), "E_blend": mean(E_blend), "E_cta": mean(E_cta),
                             "E_kept_after_warp_cull": mean(E_kept), "pixels": W * H},
             "roofline": roof,
-            # ours per frame: k_preprocess, 4 x k_onesweep, k_entry_scan, k_entries, k_big_entries,
-            # k_l1_count, k_l1_scan, k_l1_emit, k_l2_count, k_l2_scan, k_l2_write, k_render
-            "gpu_launches": n_timed * 15,
+            # ours per frame: k_preprocess, 4 x k_onesweep, k_escan_reduce, k_escan_apply, k_entries,
+            # k_big_entries, k_l1_count, k_l1_scan, k_l1_emit, k_l2_count, k_l2_scan, k_l2_write, k_render
+            "gpu_launches": n_timed * 16,
             "clocks": clk,
             "e2e": e2e,
             "prune_score": score_info,

@@ -5,7 +5,7 @@
 // the sorted pair list is a STABLE partition of that sequence's pairs by tile.  It is built
 // in two levels, on the super-tile entries of ss_tilegeom.cuh (one entry per 4x4-tile
 // super-tile a Gaussian touches, with a 16-bit mask of its tiles there):
-//   k_entry_scan  InclusiveSum over the Gaussians in depth order, of their entry
+//   k_escan_*     InclusiveSum over the Gaussians in depth order, of their entry
 //                 counts: every entry gets a global index, so the work of the next steps
 //                 is cut into equal-size units of entries (near Gaussians cover hundreds of
 //                 super-tiles; chunks of Gaussians would be badly unbalanced).
@@ -35,100 +35,89 @@ constexpr int kL2Block = kL2Threads * kL2PerThread;  // entries per level-2 bloc
 static_assert(kL2Block == kL2BlockEntries, "level-2 block size");
 
 // ---------------------------------------------------------------- entry scan
-// Warp-cooperative decoupled look-back over block tickets: lane l inspects the status of
-// tile (bid - 1 - l - 32 j); the walk stops at the nearest inclusive prefix.  Returns the
-// exclusive prefix of tile bid.  Called by one full warp.
-__device__ __forceinline__ uint32_t warp_lookback(const uint32_t *lookback, uint32_t bid, int lane) {
-    const volatile uint32_t *lb = lookback;
-    uint32_t acc = 0;
-    int base = (int)bid - 1;
-    for (;;) {
-        const int idx = base - lane;
-        uint32_t v;
-        int first_inc;
-        for (;;) {  // spin until every status up to the nearest inclusive one is published
-            v = idx >= 0 ? lb[idx] : kFlagInc;  // before tile 0: a virtual inclusive 0
-            const uint32_t inc = __ballot_sync(0xffffffffu, (v & ~kValMask) == kFlagInc);
-            const uint32_t zero = __ballot_sync(0xffffffffu, (v & ~kValMask) == 0);
-            first_inc = inc ? __ffs(inc) - 1 : 32;
-            const uint32_t need = first_inc == 32 ? 0xffffffffu : (0xffffffffu >> (31 - first_inc));
-            if (!(zero & need)) break;
-        }
-        uint32_t part = (lane <= first_inc) ? (v & kValMask) : 0u;
+// Reduce-then-scan over tiles of kScanTile Gaussians (no look-back chain): k_escan_reduce
+// sums every tile; k_escan_apply scans its tile on top of the sum of all earlier tiles (each
+// CTA adds the few hundred tile sums before it itself).
+
+__device__ __forceinline__ void scan_load(const uint32_t *__restrict__ one, size_t k0, uint32_t nv, uint32_t *v) {
+    if (k0 + kScanItems <= nv) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(one + k0);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        acc += part;
-        if (first_inc < 32) return acc;
-        base -= 32;
+        for (int q = 0; q < kScanItems / 4; ++q) {
+            const uint4 x = src[q];
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = x.z;
+            v[4 * q + 3] = x.w;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kScanItems; ++q) v[q] = k0 + q < nv ? one[k0 + q] : 0u;
     }
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_escan_reduce(const uint32_t *__restrict__ n_visible,
+                                                               const uint32_t *__restrict__ one,
+                                                               uint32_t *__restrict__ tile_sum) {
+    pdl_enter();
+    __shared__ uint32_t s_warp[8];
+    const uint32_t nv = *n_visible;
+    const size_t base = (size_t)blockIdx.x * kScanTile;
+    if (base >= nv) return;
+    uint32_t v[kScanItems];
+    scan_load(one, base + (size_t)threadIdx.x * kScanItems, nv, v);
+    uint32_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) sum += v[q];
+    uint32_t total;
+    block_exclusive_scan_256(sum, s_warp, total);
+    if (threadIdx.x == 0) tile_sum[blockIdx.x] = total;
 }
 
 // eoff[k] = sum of one[0..k) over the nv visible Gaussians in depth order; total E; the
 // overflow flag (P, summed by ss_preprocess, > capacity).
-__global__ void __launch_bounds__(kScanThreads) k_entry_scan(const uint32_t *__restrict__ n_visible,
-                                                             const uint32_t *__restrict__ one,
-                                                             uint32_t *__restrict__ eoff,
-                                                             uint32_t *lookback, uint32_t *ticket,
-                                                             const uint32_t *__restrict__ total_pairs, uint32_t cap,
-                                                             uint32_t *__restrict__ total_entries,
-                                                             uint32_t *__restrict__ overflow) {
+__global__ void __launch_bounds__(kScanThreads) k_escan_apply(const uint32_t *__restrict__ n_visible,
+                                                              const uint32_t *__restrict__ one,
+                                                              const uint32_t *__restrict__ tile_sum,
+                                                              uint32_t *__restrict__ eoff,
+                                                              const uint32_t *__restrict__ total_pairs, uint32_t cap,
+                                                              uint32_t *__restrict__ total_entries,
+                                                              uint32_t *__restrict__ overflow) {
     pdl_enter();
     __shared__ uint32_t s_warp[8];
-    __shared__ uint32_t s_bid, s_base;
     const uint32_t nv = *n_visible;
-    const int tid = threadIdx.x, lane = tid & 31;
+    const int tid = threadIdx.x;
     if (blockIdx.x == 0 && tid == 0) *overflow = *total_pairs > cap ? 1u : 0u;
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) s_bid = atomicAdd(ticket, 1u);
-        __syncthreads();
-        const uint32_t bid = s_bid;
-        const size_t base = (size_t)bid * kScanTile;
-        if (base >= nv) break;
-        const size_t k0 = base + (size_t)tid * kScanItems;
-        uint32_t v[kScanItems];
-        uint32_t sum = 0;
-        if (k0 + kScanItems <= nv) {
-            const uint4 *src = reinterpret_cast<const uint4 *>(one + k0);
+    const size_t base = (size_t)blockIdx.x * kScanTile;
+    if (base >= nv) return;
+    // the sum of the earlier tiles
+    uint32_t pre = 0;
+    for (uint32_t b = tid; b < blockIdx.x; b += kScanThreads) pre += tile_sum[b];
+    uint32_t tile_base;
+    block_exclusive_scan_256(pre, s_warp, tile_base);
+    __syncthreads();
+    const size_t k0 = base + (size_t)tid * kScanItems;
+    uint32_t v[kScanItems];
+    scan_load(one, k0, nv, v);
+    uint32_t sum = 0;
 #pragma unroll
-            for (int q = 0; q < kScanItems / 4; ++q) {
-                const uint4 x = src[q];
-                v[4 * q] = x.x;
-                v[4 * q + 1] = x.y;
-                v[4 * q + 2] = x.z;
-                v[4 * q + 3] = x.w;
-            }
-        } else {
+    for (int q = 0; q < kScanItems; ++q) sum += v[q];
+    uint32_t total;
+    uint32_t run = tile_base + block_exclusive_scan_256(sum, s_warp, total);
+    if (tid == 0 && base + kScanTile >= nv) *total_entries = tile_base + total;
+    // blocked -> striped through shared memory, so that the stores are coalesced
+    __shared__ uint32_t s_out[kScanTile];
 #pragma unroll
-            for (int q = 0; q < kScanItems; ++q) v[q] = k0 + q < nv ? one[k0 + q] : 0u;
-        }
+    for (int q = 0; q < kScanItems; ++q) {
+        s_out[tid * kScanItems + ((q + tid) & (kScanItems - 1))] = run;  // rotated: no bank conflicts
+        run += v[q];
+    }
+    __syncthreads();
 #pragma unroll
-        for (int q = 0; q < kScanItems; ++q) sum += v[q];
-        uint32_t total;
-        uint32_t run = block_exclusive_scan_256(sum, s_warp, total);
-        if (tid < 32) {
-            if (tid == 0) {
-                volatile uint32_t *lbv = lookback;
-                lbv[bid] = (bid == 0 ? kFlagInc : kFlagAgg) | total;
-            }
-            const uint32_t acc = bid == 0 ? 0u : warp_lookback(lookback, bid, lane);
-            if (tid == 0) {
-                if (bid > 0) {
-                    volatile uint32_t *lbv = lookback;
-                    lbv[bid] = kFlagInc | (acc + total);
-                }
-                s_base = acc;
-                if (base + kScanTile >= nv) *total_entries = acc + total;
-            }
-        }
-        __syncthreads();
-        run += s_base;
-#pragma unroll
-        for (int q = 0; q < kScanItems; ++q) {
-            const size_t k = k0 + q;
-            if (k < nv) eoff[k] = run;
-            run += v[q];
-        }
+    for (int q = 0; q < kScanItems; ++q) {
+        const uint32_t j = (uint32_t)q * kScanThreads + tid;  // item j of the tile
+        const uint32_t t = j / kScanItems, r = j % kScanItems;
+        if (base + j < nv) eoff[base + j] = s_out[t * kScanItems + ((r + t) & (kScanItems - 1))];
     }
 }
 
@@ -676,11 +665,11 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
     }
     uint32_t *ctr = at<uint32_t>(ws, L.counters);
     const int sms = sm_count();
-    const int scan_grid = (int)L.nblk_escan < sms * 4 ? (int)L.nblk_escan : sms * 4;
-    launch_pdl(k_entry_scan, scan_grid > 0 ? scan_grid : 1, kScanThreads, 0, st, 
-        at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, L.one), at<uint32_t>(ws, L.eoff),
-        at<uint32_t>(ws, L.lb_escan), ctr + 4, at<const uint32_t>(ws, P.total_pairs), L.capacity, ctr + 8,
-        at<uint32_t>(ws, P.overflow));
+    launch_pdl(k_escan_reduce, L.nblk_escan, kScanThreads, 0, st, at<const uint32_t>(ws, P.n_visible),
+               at<const uint32_t>(ws, L.one), at<uint32_t>(ws, L.lb_escan));
+    launch_pdl(k_escan_apply, L.nblk_escan, kScanThreads, 0, st, at<const uint32_t>(ws, P.n_visible),
+               at<const uint32_t>(ws, L.one), at<const uint32_t>(ws, L.lb_escan), at<uint32_t>(ws, L.eoff),
+               at<const uint32_t>(ws, P.total_pairs), L.capacity, ctr + 8, at<uint32_t>(ws, P.overflow));
     if (L.nck_max == 0) return cudaGetLastError();
     const uint32_t *E = ctr + 8;
     int sbits = 1;

@@ -65,7 +65,7 @@ struct Layout {
     size_t hist_depth;              // uint32 [4][256]
     size_t counters;                // uint32 [16] tickets: depth passes, scans, last-CTA counters
     size_t lb_depth;                // uint32 [4][nblk_depth][256]
-    size_t lb_escan;                // uint32 [nblk_escan] look-back of the entry scan
+    size_t lb_escan;                // uint32 [nblk_escan] tile sums of the entry scan
     uint32_t nblk_depth, nblk_escan;
     uint32_t nck_max;               // level-1 chunks for `capacity` entries
     uint32_t l2_max_blocks;         // level-2 blocks for `capacity` entries

@@ -14,7 +14,7 @@
 namespace ss {
 namespace {
 
-constexpr int kBatch = 256;
+constexpr int kBatch = 128;
 
 // Shared-memory batch of gathered records, split by use: the per-warp culling box, the conic
 // (skip test), the colour.
@@ -41,7 +41,7 @@ __device__ __forceinline__ float alpha_of(float q, float sigma) {
 __device__ __forceinline__ void load_batch(Batch &s, const uint32_t *__restrict__ vals,
                                            const float4 *__restrict__ rec, uint32_t j, uint32_t end,
                                            uint32_t *s_id) {
-    if (j < end) {
+    if (threadIdx.x < kBatch && j < end) {
         const uint32_t g = vals[j];
         const float4 q0 = __ldg(rec + 3 * (size_t)g + 0);  // x, y, a, b
         const float4 q1 = __ldg(rec + 3 * (size_t)g + 1);  // c, t, sigma, hx
