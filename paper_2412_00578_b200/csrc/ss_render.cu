@@ -50,6 +50,10 @@ __device__ __forceinline__ void load_batch(Batch &s, const uint32_t *__restrict_
         s.con[threadIdx.x] = make_float4(q0.z, q0.w + q0.w, q1.x, q1.y);
         s.col[threadIdx.x] = make_float4(q2.y, q2.z, q2.w, q1.z);
         if (s_id) s_id[threadIdx.x] = g;
+    } else if (threadIdx.x < kBatch) {  // padding slot: never contributes (q <= -inf is false)
+        s.box[threadIdx.x] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        s.con[threadIdx.x] = make_float4(1.0f, 0.0f, 1.0f, __int_as_float(0xff800000));
+        s.col[threadIdx.x] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
     }
 }
 
@@ -112,12 +116,15 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
             float T = st.T[pp], C0 = st.C0[pp], C1 = st.C1[pp], C2 = st.C2[pp];
             uint32_t last = st.last[pp];
             bool done = false;
-            const int cnt = min((uint32_t)kBatch, range.y - start);
+            // the batch is walked in groups of 4; the padding slots after the last Gaussian
+            // never contribute, so no per-Gaussian bound check is needed
+            const int cnt = ((int)min((uint32_t)kBatch, range.y - start) + 3) & ~3;
             const uint32_t base = start - range.x + 1;
             // branch-free blend: a non-contributing Gaussian gets alpha = 0, which leaves T and
             // C bit-identical (T * 1 = T, fma(c, 0, C) = C), so only termination branches
-#pragma unroll 4
-            for (int k = 0; k < cnt; ++k) {
+            for (int k4 = 0; k4 < cnt && !done; k4 += 4)
+#pragma unroll
+            for (int k = k4; k < k4 + 4; ++k) {
                 const float4 bx = s.box[k];
                 const float4 cn = s.con[k];
                 const float4 cl = s.col[k];
