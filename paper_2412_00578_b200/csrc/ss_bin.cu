@@ -640,11 +640,11 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_write(const uint32_t *__restr
             s_run[tid] = run;
         }
         __syncthreads();
-        uint32_t mm = m;
-        while (mm) {
-            const int t = __ffs(mm) - 1;
-            mm &= mm - 1;
-            sorted_value[s_off[w][t] + __popc(s_bal[w][t] & lt_mask)] = v[q].x;
+        // tile by tile, so that each store instruction fills consecutive positions of one tile
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            const uint32_t bal = s_bal[w][t];
+            if ((m >> t) & 1u) sorted_value[s_off[w][t] + __popc(bal & lt_mask)] = v[q].x;
         }
         __syncthreads();
     }
