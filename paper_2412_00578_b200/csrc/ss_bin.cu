@@ -288,9 +288,11 @@ __device__ __forceinline__ void unit_bounds(uint32_t c, int w, uint32_t E, uint3
 }
 
 // Lanes holding the same key (nbits wide) as this lane, by nbits ballots; 0 for invalid lanes.
-__device__ __forceinline__ uint32_t key_peers(uint32_t key, bool valid, int nbits) {
+template <int NBITS>
+__device__ __forceinline__ uint32_t key_peers(uint32_t key, bool valid) {
     uint32_t peers = __ballot_sync(0xffffffffu, valid);
-    for (int bit = 0; bit < nbits; ++bit) {
+#pragma unroll
+    for (int bit = 0; bit < NBITS; ++bit) {
         const bool v = (key >> bit) & 1u;
         const uint32_t m = __ballot_sync(0xffffffffu, v);
         peers &= v ? m : ~m;
@@ -299,9 +301,10 @@ __device__ __forceinline__ uint32_t key_peers(uint32_t key, bool valid, int nbit
 }
 
 // Entries per (chunk, super-tile) -> M[c][s], from the staged entries.
-__global__ void __launch_bounds__(kBinWarps * 32) k_l1_count(const uint32_t *__restrict__ total_entries,
+template <int SBITS>  // super-tile id width (ballots per rank)
+__global__ void __launch_bounds__(kBinWarps * 32, 3) k_l1_count(const uint32_t *__restrict__ total_entries,
                                                               const uint32_t *__restrict__ overflow, int n_super,
-                                                              int sbits, const uint2 *__restrict__ stg,
+                                                              const uint2 *__restrict__ stg,
                                                               uint32_t *__restrict__ M) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -326,7 +329,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_l1_count(const uint32_t *__r
 #pragma unroll
     for (int q = 0; q < kPerLane; ++q) {
         const bool valid = (uint32_t)q * 32 + lane < n;
-        const uint32_t peers = key_peers(st[q], valid, sbits);
+        const uint32_t peers = key_peers<SBITS>(st[q], valid);
         if (valid && (peers & lt_mask) == 0) h[st[q]] += __popc(peers);
         __syncwarp();
     }
@@ -408,9 +411,10 @@ __global__ void __launch_bounds__(256) k_l1_scan(const uint32_t *__restrict__ to
 
 // Every entry written once, at st_base[s] + (entries of s in earlier chunks) + (in earlier
 // warps of the chunk) + its rank in the warp; the entries come from k_l1_count's staging.
-__global__ void __launch_bounds__(kBinWarps * 32) k_l1_emit(const uint32_t *__restrict__ total_entries,
+template <int SBITS>
+__global__ void __launch_bounds__(kBinWarps * 32, 3) k_l1_emit(const uint32_t *__restrict__ total_entries,
                                                              const uint32_t *__restrict__ overflow, int n_super,
-                                                             int sbits, const uint32_t *__restrict__ M,
+                                                             const uint32_t *__restrict__ M,
                                                              const uint32_t *__restrict__ st_base,
                                                              const uint2 *__restrict__ stg, uint2 *__restrict__ ent) {
     pdl_enter();
@@ -433,12 +437,13 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_l1_emit(const uint32_t *__re
     }
     __syncthreads();
     uint32_t *h = hist + (size_t)w * n_super;
+    uint32_t pk[kPerLane];  // peer masks, reused by the ranking pass
 #pragma unroll
     for (int q = 0; q < kPerLane; ++q) {
         const bool valid = (uint32_t)q * 32 + lane < n;
         const uint32_t st = valid ? (v[q].y & 0xFFFFu) : 0u;
-        const uint32_t peers = key_peers(st, valid, sbits);
-        if (valid && (peers & lt_mask) == 0) h[st] += __popc(peers);
+        pk[q] = key_peers<SBITS>(st, valid);
+        if (valid && (pk[q] & lt_mask) == 0) h[st] += __popc(pk[q]);
         __syncwarp();
     }
     __syncthreads();
@@ -456,7 +461,7 @@ __global__ void __launch_bounds__(kBinWarps * 32) k_l1_emit(const uint32_t *__re
     for (int q = 0; q < kPerLane; ++q) {
         const bool valid = (uint32_t)q * 32 + lane < n;
         const uint32_t st = valid ? (v[q].y & 0xFFFFu) : 0u;
-        const uint32_t peers = key_peers(st, valid, sbits);
+        const uint32_t peers = pk[q];
         uint32_t prev = 0;
         if (valid) {
             prev = h[st];
@@ -652,6 +657,24 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_write(const uint32_t *__restr
 
 size_t l1_smem_bytes(int n_super) { return (size_t)kBinWarps * n_super * 4; }
 
+template <int SBITS>
+cudaError_t launch_level1(void *ws, const Layout &L, size_t smem, const uint32_t *E, uint32_t *ctr, cudaStream_t st) {
+    const ss_layout &P = L.pub;
+    static int smem_count[64] = {0}, smem_emit[64] = {0};
+    cudaError_t e = ensure_smem(k_l1_count<SBITS>, smem, smem_count);
+    if (e == cudaSuccess) e = ensure_smem(k_l1_emit<SBITS>, smem, smem_emit);
+    if (e != cudaSuccess) return e;
+    launch_pdl(k_l1_count<SBITS>, L.nck_max, kBinWarps * 32, smem, st, E, at<const uint32_t>(ws, P.overflow),
+               L.n_super, at<const uint2>(ws, L.stg), at<uint32_t>(ws, L.bin_M));
+    launch_pdl(k_l1_scan, L.n_super, 256, 0, st, E, at<const uint32_t>(ws, P.overflow), L.n_super,
+               at<uint32_t>(ws, L.bin_M), at<uint32_t>(ws, L.st_total), at<uint32_t>(ws, L.st_base),
+               at<uint32_t>(ws, L.st_blk0), at<uint2>(ws, L.l2_blocks), ctr + 11, ctr + 9);
+    launch_pdl(k_l1_emit<SBITS>, L.nck_max, kBinWarps * 32, smem, st, E, at<const uint32_t>(ws, P.overflow),
+               L.n_super, at<const uint32_t>(ws, L.bin_M), at<const uint32_t>(ws, L.st_base),
+               at<const uint2>(ws, L.stg), at<uint2>(ws, L.ent));
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
@@ -684,19 +707,15 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
                                            at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y, L.stx,
                                            at<uint2>(ws, L.stg));
     const size_t smem = l1_smem_bytes(L.n_super);
-    static int smem_count[64] = {0}, smem_emit[64] = {0};
-    cudaError_t e = ensure_smem(k_l1_count, smem, smem_count);
-    if (e == cudaSuccess) e = ensure_smem(k_l1_emit, smem, smem_emit);
+    cudaError_t e = cudaSuccess;
+    switch (sbits <= 8 ? 8 : sbits) {
+        case 8: e = launch_level1<8>(ws, L, smem, E, ctr, st); break;
+        case 9: e = launch_level1<9>(ws, L, smem, E, ctr, st); break;
+        case 10: e = launch_level1<10>(ws, L, smem, E, ctr, st); break;
+        case 11: e = launch_level1<11>(ws, L, smem, E, ctr, st); break;
+        default: e = launch_level1<12>(ws, L, smem, E, ctr, st); break;
+    }
     if (e != cudaSuccess) return e;
-    launch_pdl(k_l1_count, L.nck_max, kBinWarps * 32, smem, st, E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
-                                                        at<const uint2>(ws, L.stg), at<uint32_t>(ws, L.bin_M));
-    launch_pdl(k_l1_scan, L.n_super, 256, 0, st, E, at<const uint32_t>(ws, P.overflow), L.n_super, at<uint32_t>(ws, L.bin_M),
-                                         at<uint32_t>(ws, L.st_total), at<uint32_t>(ws, L.st_base),
-                                         at<uint32_t>(ws, L.st_blk0), at<uint2>(ws, L.l2_blocks), ctr + 11, ctr + 9);
-    launch_pdl(k_l1_emit, L.nck_max, kBinWarps * 32, smem, st, E, at<const uint32_t>(ws, P.overflow), L.n_super, sbits,
-                                                         at<const uint32_t>(ws, L.bin_M),
-                                                         at<const uint32_t>(ws, L.st_base),
-                                                         at<const uint2>(ws, L.stg), at<uint2>(ws, L.ent));
     launch_pdl(k_l2_count, L.l2_max_blocks, kL2Threads, 0, st, 
         at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super, at<const uint32_t>(ws, L.st_total),
         at<const uint32_t>(ws, L.st_base), at<const uint32_t>(ws, L.st_blk0), at<const uint2>(ws, L.l2_blocks),
