@@ -419,7 +419,11 @@ __global__ void __launch_bounds__(kBinWarps * 32, 3) k_l1_emit(const uint32_t *_
                                                              const uint2 *__restrict__ stg, uint2 *__restrict__ ent) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    uint32_t *hist = reinterpret_cast<uint32_t *>(smem_raw);
+    uint2 *stage = reinterpret_cast<uint2 *>(smem_raw);                  // [kEntChunk] by super-tile
+    uint32_t *hist = reinterpret_cast<uint32_t *>(stage + kEntChunk);    // [kBinWarps][n_super]
+    uint32_t *loff = hist + (size_t)kBinWarps * n_super;                 // [n_super] chunk-local first
+    uint32_t *gb = loff + n_super;                                       // [n_super] global first
+    __shared__ uint32_t s_warp[8];
     const uint32_t E = *total_entries, c = blockIdx.x;
     if (*overflow || c * (uint32_t)kEntChunk >= E) return;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -428,6 +432,7 @@ __global__ void __launch_bounds__(kBinWarps * 32, 3) k_l1_emit(const uint32_t *_
     uint32_t b, B0, B1;
     unit_bounds(c, w, E, b, B0, B1);
     const uint32_t n = B0 < B1 ? B1 - B0 : 0u;
+    const uint32_t n_cta = min((uint32_t)kEntChunk, E - c * (uint32_t)kEntChunk);
     constexpr int kPerLane = kEntWarp / 32;
     uint2 v[kPerLane];
 #pragma unroll
@@ -447,14 +452,30 @@ __global__ void __launch_bounds__(kBinWarps * 32, 3) k_l1_emit(const uint32_t *_
         __syncwarp();
     }
     __syncthreads();
-    for (int s = threadIdx.x; s < n_super; s += blockDim.x) {
-        uint32_t run = st_base[s] + M[(size_t)c * n_super + s];
+    // chunk-local layout by super-tile: loff[s] = entries of super-tiles < s in this chunk;
+    // warp w's entries of s start at loff[s] + (entries of s in warps < w)
+    const int per = (n_super + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int s0 = min(n_super, (int)threadIdx.x * per), s1 = min(n_super, s0 + per);
+    uint32_t local = 0;
+    for (int s = s0; s < s1; ++s) {
+        uint32_t tot = 0;
+#pragma unroll
+        for (int q = 0; q < kBinWarps; ++q) tot += hist[(size_t)q * n_super + s];
+        local += tot;
+    }
+    uint32_t cta_total;
+    uint32_t run0 = block_exclusive_scan_256(local, s_warp, cta_total);
+    for (int s = s0; s < s1; ++s) {
+        loff[s] = run0;
+        gb[s] = st_base[s] + M[(size_t)c * n_super + s];
+        uint32_t run = run0;
 #pragma unroll
         for (int q = 0; q < kBinWarps; ++q) {
             const uint32_t x = hist[(size_t)q * n_super + s];
             hist[(size_t)q * n_super + s] = run;
             run += x;
         }
+        run0 = run;
     }
     __syncthreads();
 #pragma unroll
@@ -465,11 +486,18 @@ __global__ void __launch_bounds__(kBinWarps * 32, 3) k_l1_emit(const uint32_t *_
         uint32_t prev = 0;
         if (valid) {
             prev = h[st];
-            ent[prev + __popc(peers & lt_mask)] = make_uint2(v[q].x, v[q].y >> 16);
+            stage[prev + __popc(peers & lt_mask)] = v[q];
         }
         __syncwarp();
         if (valid && (peers & lt_mask) == 0) h[st] = prev + __popc(peers);
         __syncwarp();
+    }
+    __syncthreads();
+    // write-out in chunk-local order: runs of one super-tile land on consecutive positions
+    for (uint32_t i = threadIdx.x; i < n_cta; i += blockDim.x) {
+        const uint2 e = stage[i];
+        const uint32_t s = e.y & 0xFFFFu;
+        ent[gb[s] + (i - loff[s])] = make_uint2(e.x, e.y >> 16);
     }
 }
 
@@ -661,15 +689,16 @@ template <int SBITS>
 cudaError_t launch_level1(void *ws, const Layout &L, size_t smem, const uint32_t *E, uint32_t *ctr, cudaStream_t st) {
     const ss_layout &P = L.pub;
     static int smem_count[64] = {0}, smem_emit[64] = {0};
+    const size_t smem_e = (size_t)kEntChunk * 8 + ((size_t)kBinWarps + 2) * L.n_super * 4;
     cudaError_t e = ensure_smem(k_l1_count<SBITS>, smem, smem_count);
-    if (e == cudaSuccess) e = ensure_smem(k_l1_emit<SBITS>, smem, smem_emit);
+    if (e == cudaSuccess) e = ensure_smem(k_l1_emit<SBITS>, smem_e, smem_emit);
     if (e != cudaSuccess) return e;
     launch_pdl(k_l1_count<SBITS>, L.nck_max, kBinWarps * 32, smem, st, E, at<const uint32_t>(ws, P.overflow),
                L.n_super, at<const uint2>(ws, L.stg), at<uint32_t>(ws, L.bin_M));
     launch_pdl(k_l1_scan, L.n_super, 256, 0, st, E, at<const uint32_t>(ws, P.overflow), L.n_super,
                at<uint32_t>(ws, L.bin_M), at<uint32_t>(ws, L.st_total), at<uint32_t>(ws, L.st_base),
                at<uint32_t>(ws, L.st_blk0), at<uint2>(ws, L.l2_blocks), ctr + 11, ctr + 9);
-    launch_pdl(k_l1_emit<SBITS>, L.nck_max, kBinWarps * 32, smem, st, E, at<const uint32_t>(ws, P.overflow),
+    launch_pdl(k_l1_emit<SBITS>, L.nck_max, kBinWarps * 32, smem_e, st, E, at<const uint32_t>(ws, P.overflow),
                L.n_super, at<const uint32_t>(ws, L.bin_M), at<const uint32_t>(ws, L.st_base),
                at<const uint2>(ws, L.stg), at<uint2>(ws, L.ent));
     return cudaGetLastError();
