@@ -8,6 +8,8 @@
 // function on the same values (R1) and are exact for the stored conic.
 //
 // P:n = /root/reference/PAPER.md line n.
+#include <cuda_pipeline.h>
+
 #include "ss_tilegeom.cuh"
 
 namespace ss {
@@ -65,6 +67,8 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
     const float limy = cam.clip * ((0.5f * (float)cam.H) / cam.fy);
     const int stx = (cam.tiles_x + kSuper - 1) / kSuper;
     const int lane = threadIdx.x & 31;
+    extern __shared__ float4 s_sh[];                  // per thread: one SH block (+1 float4 pad)
+    float4 *my_sh = s_sh + (size_t)threadIdx.x * (NP + 1);
     // warp-uniform grid-stride loop (the tall-Gaussian phase below is warp-collective)
     for (int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += gridDim.x * blockDim.x) {
         const int i = i0 + lane;
@@ -153,6 +157,13 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
                                         cam.tiles_y);
                     } else {
                         R = rect_of_snug(snug, cam.tiles_x, cam.tiles_y);
+                    }
+                    if (R.x < R.y && R.z < R.w) {
+                        // the Gaussian has (almost surely) tiles: its SH block is copied to shared
+                        // memory now (cp.async), overlapping the tile sweep below
+#pragma unroll
+                        for (int p = 0; p < NP; ++p) __pipeline_memcpy_async(my_sh + p, sh + (size_t)i * NP + p, 16);
+                        __pipeline_commit();
                     }
                     if (mode == SS_BIN_ACCUTILE) {
                         Sweep w;
@@ -251,9 +262,10 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             float Y[16];
             sh_basis<DEG>(dx * il, dy * il, dz * il, Y);
             float hc[NP * 4];
+            __pipeline_wait_prior(0);  // the SH block copied before the tile sweep
 #pragma unroll
             for (int p = 0; p < NP; ++p) {
-                const float4 v = __ldg(sh + (size_t)i * NP + p);  // the Gaussian's contiguous SH block
+                const float4 v = my_sh[p];
                 hc[4 * p + 0] = v.x;
                 hc[4 * p + 1] = v.y;
                 hc[4 * p + 2] = v.z;
@@ -306,6 +318,7 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__re
             ++my_vis;
             my_pairs += count;
         } else if (valid) {
+            __pipeline_wait_prior(0);  // a copy issued for a Gaussian that ended without tiles
             depth_key[i] = kNoTiles;
             gne[i] = 0u;
         }
@@ -345,12 +358,29 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
         reinterpret_cast<const float4 *>(sc.rot), reinterpret_cast<const float4 *>(sc.sh), cam, mode,         \
         at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key), at<uint32_t>(ws, L.gne), \
         at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs)
+    const int NPd = ((sc.sh_degree + 1) * (sc.sh_degree + 1) * 3 + 3) / 4;
+    const size_t smem = (size_t)256 * (NPd + 1) * 16;  // per-thread SH staging (cp.async)
+    static int done[4][64] = {{0}};
+    cudaError_t e = cudaSuccess;
     switch (sc.sh_degree) {
-        case 0: launch_pdl(k_preprocess<0>, grid, 256, 0, st, SS_PRE_ARGS); break;
-        case 1: launch_pdl(k_preprocess<1>, grid, 256, 0, st, SS_PRE_ARGS); break;
-        case 2: launch_pdl(k_preprocess<2>, grid, 256, 0, st, SS_PRE_ARGS); break;
-        default: launch_pdl(k_preprocess<3>, grid, 256, 0, st, SS_PRE_ARGS); break;
+        case 0:
+            e = ensure_smem(k_preprocess<0>, smem, done[0]);
+            if (e == cudaSuccess) launch_pdl(k_preprocess<0>, grid, 256, smem, st, SS_PRE_ARGS);
+            break;
+        case 1:
+            e = ensure_smem(k_preprocess<1>, smem, done[1]);
+            if (e == cudaSuccess) launch_pdl(k_preprocess<1>, grid, 256, smem, st, SS_PRE_ARGS);
+            break;
+        case 2:
+            e = ensure_smem(k_preprocess<2>, smem, done[2]);
+            if (e == cudaSuccess) launch_pdl(k_preprocess<2>, grid, 256, smem, st, SS_PRE_ARGS);
+            break;
+        default:
+            e = ensure_smem(k_preprocess<3>, smem, done[3]);
+            if (e == cudaSuccess) launch_pdl(k_preprocess<3>, grid, 256, smem, st, SS_PRE_ARGS);
+            break;
     }
+    if (e != cudaSuccess) return e;
 #undef SS_PRE_ARGS
     return cudaGetLastError();
 }
