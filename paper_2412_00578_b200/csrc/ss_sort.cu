@@ -79,13 +79,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restric
             const size_t idx = wbase + (size_t)j * 32;
             const bool valid = idx < n && (!FILTER || key[j] != kNoTiles);
             const uint32_t d = digit_of(key[j], shift);
-            uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-            for (int b = 0; b < 8; ++b) {
-                const bool bit = (d >> b) & 1u;
-                const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-                peers &= bit ? bal : ~bal;
-            }
+            const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 256u + (uint32_t)lane);
             const uint32_t lt = __popc(peers & lanemask_lt);
             uint32_t prev = 0;
             if (valid) prev = s_whist[warp][d];
