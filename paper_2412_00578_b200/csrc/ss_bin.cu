@@ -561,65 +561,57 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_count(const uint32_t *__restr
     }
 }
 
-// Per super-tile and tile, the exclusive prefix over the super-tile's level-2 blocks (in BC)
-// and the tile totals; then the exclusive scan over the tiles in row-major order (tile_base,
-// ranges = identifyTileRanges).  Block blk's pairs of tile t start at tile_base[t] + BC[blk][t].
-__global__ void __launch_bounds__(1024) k_l2_scan(const uint32_t *__restrict__ overflow, int stx, int tiles_x,
-                                                  int tiles_y, int n_super, const uint32_t *__restrict__ st_total,
-                                                  const uint32_t *__restrict__ st_blk0, uint32_t *__restrict__ BC,
-                                                  uint32_t *__restrict__ tile_count, uint32_t *__restrict__ tile_base,
-                                                  uint2 *__restrict__ ranges) {
+// Per super-tile and tile (one thread each, spread over the grid), the exclusive prefix over
+// the super-tile's level-2 blocks (in BC) and the tile totals; the last CTA to finish scans
+// the tiles in row-major order (tile_base, ranges = identifyTileRanges).  Block blk's pairs of
+// tile t start at tile_base[t] + BC[blk][t].
+__global__ void __launch_bounds__(256) k_l2_scan(const uint32_t *__restrict__ overflow, int stx, int tiles_x,
+                                                 int tiles_y, int n_super, const uint32_t *__restrict__ st_total,
+                                                 const uint32_t *__restrict__ st_blk0, uint32_t *__restrict__ BC,
+                                                 uint32_t *__restrict__ tile_count, uint32_t *__restrict__ tile_base,
+                                                 uint2 *__restrict__ ranges, uint32_t *done) {
     pdl_enter();
-    __shared__ uint32_t s_warp[32];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    __shared__ uint32_t s_warp[8];
+    __shared__ bool s_last;
+    const int tid = threadIdx.x;
     const bool ovf = *overflow != 0;
-    for (int j = tid; j < n_super * 16; j += 1024) {
+    const int j = blockIdx.x * blockDim.x + tid;
+    if (j < n_super * 16) {
         const int sidx = j >> 4, bit = j & 15;
-        if (!tile_in_grid(sidx, bit, stx, tiles_x, tiles_y)) continue;
-        uint32_t tot = 0;
-        if (!ovf) {
-            const uint32_t nbs = (st_total[sidx] + kL2Block - 1) / kL2Block;
-            uint32_t *col = BC + (size_t)st_blk0[sidx] * 16 + bit;
-            for (uint32_t q0 = 0; q0 < nbs; q0 += 8) {  // eight independent loads in flight
-                uint32_t x[8];
+        if (tile_in_grid(sidx, bit, stx, tiles_x, tiles_y)) {
+            uint32_t tot = 0;
+            if (!ovf) {
+                const uint32_t nbs = (st_total[sidx] + kL2Block - 1) / kL2Block;
+                uint32_t *col = BC + (size_t)st_blk0[sidx] * 16 + bit;
+                for (uint32_t q0 = 0; q0 < nbs; q0 += 8) {  // eight independent loads in flight
+                    uint32_t x[8];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) x[q] = q0 + q < nbs ? col[(size_t)(q0 + q) * 16] : 0u;
+                    for (int q = 0; q < 8; ++q) x[q] = q0 + q < nbs ? col[(size_t)(q0 + q) * 16] : 0u;
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    if (q0 + q < nbs) col[(size_t)(q0 + q) * 16] = tot;
-                    tot += x[q];
+                    for (int q = 0; q < 8; ++q) {
+                        if (q0 + q < nbs) col[(size_t)(q0 + q) * 16] = tot;
+                        tot += x[q];
+                    }
                 }
             }
+            tile_count[tile_of(sidx, bit, stx, tiles_x)] = tot;
         }
-        tile_count[tile_of(sidx, bit, stx, tiles_x)] = tot;
     }
+    __threadfence();
     __syncthreads();
+    if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
     const int T = tiles_x * tiles_y;
-    const int per = (T + 1023) / 1024;
+    const int per = (T + 255) / 256;
     const int t0 = min(T, tid * per), t1 = min(T, t0 + per);
     uint32_t local = 0;
-    for (int t = t0; t < t1; ++t) local += tile_count[t];
-    uint32_t x = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_warp[wid] = x;
-    __syncthreads();
-    if (wid == 0) {
-        uint32_t v = s_warp[lane];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-            if (lane >= o) v += y;
-        }
-        s_warp[lane] = v;
-    }
-    __syncthreads();
-    uint32_t run = (wid ? s_warp[wid - 1] : 0u) + x - local;
+    for (int t = t0; t < t1; ++t) local += __ldcg(tile_count + t);
+    uint32_t P;
+    uint32_t run = block_exclusive_scan_256(local, s_warp, P);
     for (int t = t0; t < t1; ++t) {
-        const uint32_t c = tile_count[t];
+        const uint32_t c = __ldcg(tile_count + t);
         tile_base[t] = run;
         ranges[t] = c ? make_uint2(run, run + c) : make_uint2(0u, 0u);
         run += c;
@@ -749,10 +741,10 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
         at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super, at<const uint32_t>(ws, L.st_total),
         at<const uint32_t>(ws, L.st_base), at<const uint32_t>(ws, L.st_blk0), at<const uint2>(ws, L.l2_blocks),
         ctr + 11, at<const uint2>(ws, L.ent), at<uint32_t>(ws, L.l2_BC));
-    launch_pdl(k_l2_scan, 1, 1024, 0, st, at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super,
-                                  at<const uint32_t>(ws, L.st_total), at<const uint32_t>(ws, L.st_blk0),
-                                  at<uint32_t>(ws, L.l2_BC), at<uint32_t>(ws, P.tile_count),
-                                  at<uint32_t>(ws, L.tile_base), at<uint2>(ws, P.ranges));
+    launch_pdl(k_l2_scan, (L.n_super * 16 + 255) / 256, 256, 0, st, at<const uint32_t>(ws, P.overflow), L.stx,
+               P.tiles_x, P.tiles_y, L.n_super, at<const uint32_t>(ws, L.st_total), at<const uint32_t>(ws, L.st_blk0),
+               at<uint32_t>(ws, L.l2_BC), at<uint32_t>(ws, P.tile_count), at<uint32_t>(ws, L.tile_base),
+               at<uint2>(ws, P.ranges), ctr + 10);
     return cudaGetLastError();
 }
 
