@@ -1,0 +1,88 @@
+"""Frames/s and pairs/frame of every BASELINE.json configuration and tile test (GPU, 1 rank).
+
+    python scripts/sweep.py [--steps 3] [--views 32] > profiles/r01_sweep.jsonl
+
+One JSON line per (workload, mode): the forward path a1-a6 through the public API, V views
+per step, K timed steps (CUDA events, L2 flushed between steps, 2 warm-up steps), plus the
+pruned-model regime (BASELINE config 5: U~ over every view, then the prune step removing 90%
+of the Gaussians, AccuTile).  The speed-ups of SnugBox and AccuTile over the 3-sigma baseline
+are the quantities the paper reports as 1.82x / 1.99x on an RTX A5000.
+"""
+import argparse
+import json
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2412_00578_b200 import synth  # noqa: E402
+from paper_2412_00578_b200.raster import DeviceScene, Rasterizer, camera_struct, prune  # noqa: E402
+
+
+def measure(ds, cams, mode, steps, views):
+    W, H = cams[0].width, cams[0].height
+    rz = Rasterizer(ds, W, H, mode=mode, capacity=max(1024, 4 * ds.n))
+    vs = list(range(0, len(cams), max(1, len(cams) // views)))[:views]
+    pairs = []
+    for v in vs:
+        rz.ensure_capacity(cams[v])
+    for v in vs:
+        rz.prepare(cams[v])
+        pairs.append(rz.totals()["pairs"])
+    rz._alloc(int(max(pairs) * 1.02) + 4096)
+    cs = [camera_struct(cams[v]) for v in vs]
+    out = torch.empty((3, H, W), dtype=torch.float32, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream()
+    ms = []
+    for k in range(steps + 2):
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        for c in cs:
+            rz.prepare(c)
+            rz.render(out=out)
+        b.record(st)
+        torch.cuda.synchronize()
+        if k >= 2:
+            ms.append(a.elapsed_time(b))
+    del rz
+    return {"fps": len(cs) * len(ms) / (sum(ms) / 1e3), "pairs_per_frame": float(np.mean(pairs)),
+            "views": len(cs), "steps": len(ms)}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--views", type=int, default=32)
+    args = ap.parse_args()
+    for name in ["mnr360-3m", "truck", "garden", "playroom"]:
+        scene, cams = synth.make_workload(name)
+        ds = DeviceScene.from_host(scene)
+        res = {}
+        for mode in ["3sigma", "snugbox", "accutile"]:
+            res[mode] = measure(ds, cams, mode, args.steps, args.views)
+            print(json.dumps({"workload": name, "n": scene.n, "mode": mode, **res[mode]}), flush=True)
+        base = res["3sigma"]["fps"]
+        print(json.dumps({"workload": name, "speedup_vs_3sigma": {m: res[m]["fps"] / base for m in res},
+                          "pairs_ratio_3sigma_over": {m: res["3sigma"]["pairs_per_frame"] / res[m]["pairs_per_frame"]
+                                                      for m in res}}), flush=True)
+        if name == "mnr360-3m":  # pruned-model regime: score all views, drop 90%, AccuTile
+            rz = Rasterizer(ds, cams[0].width, cams[0].height, mode="accutile", capacity=4 * scene.n)
+            score = torch.zeros(scene.n, dtype=torch.float64, device="cuda")
+            for cam in cams:
+                rz.ensure_capacity(cam)
+                rz.prepare(cam)
+                rz.prune_score(score)
+            del rz
+            pds, _ = prune(ds, score, 0.9)
+            r = measure(pds, cams, "accutile", args.steps, args.views)
+            print(json.dumps({"workload": name + "-pruned0.9", "n": pds.n, "mode": "accutile", **r,
+                              "speedup_vs_unpruned_accutile": r["fps"] / res["accutile"]["fps"]}), flush=True)
+        del ds
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
