@@ -42,10 +42,12 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *Y) {
 }
 
 // ---------------------------------------------------------------- a1 preprocess kernel
+constexpr int kPreThreads = 256;  // CTA size
+constexpr int kPreBlocks = 2;     // CTAs per SM the register budget is sized for (128 registers)
 // One thread per Gaussian ("each thread processes a single Gaussian"), persistent
 // grid-stride loop so each CTA flushes its depth-digit histograms once.
 template <int DEG>
-__global__ void __launch_bounds__(256, 2) k_preprocess(int n, const float4 *__restrict__ mean_opac,
+__global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, const float4 *__restrict__ mean_opac,
                                                     const float4 *__restrict__ scale, const float4 *__restrict__ rot,
                                                     const float4 *__restrict__ sh, CamArgs cam, int mode,
                                                     float4 *__restrict__ rec, uint4 *__restrict__ erec,
@@ -351,33 +353,34 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
     const ss_layout &P = L.pub;
     if (sc.n == 0) return cudaSuccess;
     const int sms = sm_count();
-    const int blocks_needed = (sc.n + 255) / 256;
-    const int grid = blocks_needed < sms * 8 ? blocks_needed : sms * 8;
+    const int blocks_needed = (sc.n + kPreThreads - 1) / kPreThreads;
+    const int resident = sms * kPreBlocks * 4;  // four rounds of resident CTAs
+    const int grid = blocks_needed < resident ? blocks_needed : resident;
 #define SS_PRE_ARGS                                                                                       \
     sc.n, reinterpret_cast<const float4 *>(sc.mean_opac), reinterpret_cast<const float4 *>(sc.scale),         \
         reinterpret_cast<const float4 *>(sc.rot), reinterpret_cast<const float4 *>(sc.sh), cam, mode,         \
         at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key), at<uint32_t>(ws, L.gne), \
         at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs)
     const int NPd = ((sc.sh_degree + 1) * (sc.sh_degree + 1) * 3 + 3) / 4;
-    const size_t smem = (size_t)256 * (NPd + 1) * 16;  // per-thread SH staging (cp.async)
+    const size_t smem = (size_t)kPreThreads * (NPd + 1) * 16;  // per-thread SH staging (cp.async)
     static int done[4][64] = {{0}};
     cudaError_t e = cudaSuccess;
     switch (sc.sh_degree) {
         case 0:
             e = ensure_smem(k_preprocess<0>, smem, done[0]);
-            if (e == cudaSuccess) launch_pdl(k_preprocess<0>, grid, 256, smem, st, SS_PRE_ARGS);
+            if (e == cudaSuccess) launch_pdl(k_preprocess<0>, grid, kPreThreads, smem, st, SS_PRE_ARGS);
             break;
         case 1:
             e = ensure_smem(k_preprocess<1>, smem, done[1]);
-            if (e == cudaSuccess) launch_pdl(k_preprocess<1>, grid, 256, smem, st, SS_PRE_ARGS);
+            if (e == cudaSuccess) launch_pdl(k_preprocess<1>, grid, kPreThreads, smem, st, SS_PRE_ARGS);
             break;
         case 2:
             e = ensure_smem(k_preprocess<2>, smem, done[2]);
-            if (e == cudaSuccess) launch_pdl(k_preprocess<2>, grid, 256, smem, st, SS_PRE_ARGS);
+            if (e == cudaSuccess) launch_pdl(k_preprocess<2>, grid, kPreThreads, smem, st, SS_PRE_ARGS);
             break;
         default:
             e = ensure_smem(k_preprocess<3>, smem, done[3]);
-            if (e == cudaSuccess) launch_pdl(k_preprocess<3>, grid, 256, smem, st, SS_PRE_ARGS);
+            if (e == cudaSuccess) launch_pdl(k_preprocess<3>, grid, kPreThreads, smem, st, SS_PRE_ARGS);
             break;
     }
     if (e != cudaSuccess) return e;
