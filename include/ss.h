@@ -106,16 +106,19 @@ typedef struct {
  * Records of a Gaussian with >= 1 tile (written only for those):
  *   rec  (48 B, render): q0 = (x2d, y2d, a, b), q1 = (c, t, sigma, 0), q2 = (0, r, g, b)
  *        (a, b, c) = conic Sigma_2D^-1 (Eq. 10); t = 2 log(255 sigma) (Eq. 11)
- *   erec (64 B, emission): e0 = (count, info, aux0, aux1), e1..e3 = super-tile entries 0..11;
- *        info = inline << 8 | columns << 9 | AccuTile << 10 | entries << 11; an entry is
- *        super-tile id (16 b) | mask of its 4x4 tiles << 16 (bit (y&3)*4 + (x&3)); aux = t as
- *        float64 bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1) (3-sigma / SnugBox).
+ *   erec (32 B, emission, one sector): (count, info, p0..p5); the payload holds the
+ *        non-empty line spans (tmin | tmax << 9 | line << 18) of an AccuTile set of at most 6
+ *        lines, or up to 6 super-tile entries (super-tile id | mask of its 4x4 tiles << 16,
+ *        bit (y&3)*4 + (x&3)), or -- for a Gaussian with more entries -- aux = t as float64
+ *        bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1) in p0, p1; info = span
+ *        count | entries-inline 0x100 | columns 0x200 | AccuTile 0x400 | spans-inline 0x800 |
+ *        entries << 12.
  * Depth lives in depth_key (float bits, 0xFFFFFFFF = no tiles).  The pairs are never
  * stored unsorted: ss_sort writes each one once, at its sorted position (Gaussian index,
  * uint32, in sorted_value; its tile is given by ranges, its depth by depth_key). */
 typedef struct {
     size_t rec;           /* float4 [3n]  render records                                      */
-    size_t erec;          /* uint4  [4n]  emission records                                    */
+    size_t erec;          /* uint4  [2n]  emission records                                    */
     size_t depth_key;     /* uint32 [n]   float bits of depth, 0xFFFFFFFF = no tiles          */
     size_t order;         /* uint32 [n]   visible Gaussians in (depth, index) order           */
     size_t sorted_value;  /* uint32 [capacity] Gaussian ids sorted by (tile, depth, index)    */

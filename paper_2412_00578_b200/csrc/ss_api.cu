@@ -37,7 +37,7 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
         return o;
     };
     P.rec = take(48 * N);
-    P.erec = take(64 * N);
+    P.erec = take(32 * N);
     P.depth_key = take(4 * N);
     P.order = take(4 * N);
     L->dkA = take(4 * N);

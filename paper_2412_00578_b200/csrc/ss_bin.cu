@@ -131,8 +131,8 @@ __device__ __forceinline__ void put_entry(uint2 *__restrict__ stg, uint32_t e, u
 // Entries of a Gaussian whose line spans are stored in its emission record (AccuTile, at most
 // kLaneRows lines): the band accumulator over the spans, in the count's order.
 __device__ __forceinline__ void span_entries(uint2 *__restrict__ stg, uint32_t g, uint32_t eo, uint32_t info,
-                                             const uint4 &e1, const uint4 &e2, int stx) {
-    const uint32_t v[6] = {e1.x, e1.y, e1.z, e1.w, e2.x, e2.y};
+                                             const uint4 &e0, const uint4 &e1, int stx) {
+    const uint32_t v[6] = {e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
     const uint32_t ns = info & 0xFFu;
     EntryAcc acc;
     acc_init(acc, (info & kInfoCols) != 0, stx);
@@ -147,8 +147,8 @@ __device__ __forceinline__ void span_entries(uint2 *__restrict__ stg, uint32_t g
 
 // Entries of a Gaussian with at most kInlineEnt entries: copied from its emission record.
 __device__ __forceinline__ void inline_entries(uint2 *__restrict__ stg, uint32_t g, uint32_t eo, uint32_t ne,
-                                               const uint4 &e1, const uint4 &e2, const uint4 &e3) {
-    const uint32_t v[kInlineEnt] = {e1.x, e1.y, e1.z, e1.w, e2.x, e2.y, e2.z, e2.w, e3.x, e3.y, e3.z, e3.w};
+                                               const uint4 &e0, const uint4 &e1) {
+    const uint32_t v[kInlineEnt] = {e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
 #pragma unroll
     for (int q = 0; q < kInlineEnt; ++q)
         if ((uint32_t)q < ne) put_entry(stg, eo + q, v[q] & 0xFFFFu, g, v[q] >> 16);
@@ -232,22 +232,20 @@ __global__ void __launch_bounds__(256) k_entries(const uint32_t *__restrict__ n_
         const uint32_t k = k0 + lane;
         const bool act = k < nv;
         uint32_t g = 0, eo = 0;
-        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0, e2 = e0, e3 = e0;
+        uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;
         if (act) {
             g = order[k];
             eo = eoff[k];
-            const uint4 *er = erec + 4 * (size_t)g;  // 64 B emission record: only the words in use
+            const uint4 *er = erec + 2 * (size_t)g;  // 32 B emission record: the words in use
             e0 = er[0];
             const uint32_t info = e0.y;
             const uint32_t words = (info & kInfoSpanInline) ? (info & 0xFFu)
                                    : (info & kInfoEntInline) ? (info >> kInfoEntShift) : 0u;
-            if (words > 0) e1 = er[1];
-            if (words > 4) e2 = er[2];
-            if (words > 8) e3 = er[3];
+            if (words > 2) e1 = er[1];
         }
         const bool spn = (e0.y & kInfoSpanInline) != 0, ent = (e0.y & kInfoEntInline) != 0;
-        if (act && spn) span_entries(stg, g, eo, e0.y, e1, e2, stx);
-        if (act && ent) inline_entries(stg, g, eo, e0.y >> kInfoEntShift, e1, e2, e3);
+        if (act && spn) span_entries(stg, g, eo, e0.y, e0, e1, stx);
+        if (act && ent) inline_entries(stg, g, eo, e0.y >> kInfoEntShift, e0, e1);
         // Gaussians with more entries than inline slots (a few hundred, the nearest ones, so
         // clustered at the front of the depth order): queued for k_big_entries, a warp each
         const bool big = act && !spn && !ent;
@@ -276,7 +274,7 @@ __global__ void __launch_bounds__(256) k_big_entries(const uint32_t *__restrict_
     for (uint32_t q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < nb; q += warps) {
         const uint32_t k = big_queue[q];
         const uint32_t g = order[k];
-        const uint4 e0 = erec[4 * (size_t)g];
+        const uint4 e0 = erec[2 * (size_t)g];
         big_entries(stg, g, eoff[k], e0.y, e0.z, e0.w, rec, tiles_x, tiles_y, stx);
     }
 }

@@ -25,7 +25,7 @@ struct CamArgs {
 constexpr int kSortThreads = 256;
 constexpr int kSortItems = 16;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys per block tile
-constexpr int kInlineEnt = 12;                         // super-tile entries stored in the emission record
+constexpr int kInlineEnt = 6;                          // super-tile entries stored in the emission record
 constexpr int kLaneRows = 6;                           // AccuTile lines a preprocess lane sweeps alone
 constexpr int kDepthPasses = 4;                        // 32-bit depth keys, 8-bit digits
 constexpr uint32_t kInfoEntInline = 0x100u;            // erec info: entries stored in the record

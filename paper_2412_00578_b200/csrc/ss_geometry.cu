@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
         bool tall = false;       // AccuTile with more than kLaneRows lines: the warp-collective phase
         // entries (or line spans) go straight to the emission record (only Gaussians with tiles
         // get one; words past the stored count are stale)
-        uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 4 * (size_t)i) + 4;
+        uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 2 * (size_t)i) + 2;
         uint32_t *span_out = ent_out;
         uint32_t n_span = 0;
         bool span_inline = false;
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
             accutile_setup((double)bx, (double)by, (double)ba, (double)bb, (double)bc, bt, cam.tiles_x, cam.tiles_y,
                            w);
             uint32_t pairs = 0, ents = 0;
-            uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 4 * (size_t)gi) + 4;
+            uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 2 * (size_t)gi) + 2;
             const int last = (w.s1 - 1) >> 2;
             for (int b0 = w.s0 >> 2; b0 <= last; b0 += 32) {
                 const int band = b0 + lane;
@@ -291,12 +291,12 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
             q[0] = make_float4(x2d, y2d, a, b);
             q[1] = make_float4(c, (float)td, mo.w, 0.0f);
             q[2] = make_float4(0.0f, rgb0, rgb1, rgb2);
-            // emission record (64 B): e0 (count, info, aux0, aux1), e1..e3 = up to 12 super-tile
-            // entries (super-tile | mask << 16) or, for AccuTile sets of at most kLaneRows lines,
-            // the non-empty line spans (tmin | tmax << 9 | line << 18); info = span count |
-            // entries-inline 0x100 | columns 0x200 | AccuTile 0x400 | spans-inline 0x800 | entries << 12;
-            // aux = t as float64 bits (AccuTile) or the packed rect (x0, x1-x0-1, y0, y1-y0-1)
-            // for the re-enumeration of Gaussians with more than kInlineEnt entries.
+            // emission record (32 B, one sector): (count, info, p0..p5); the payload p holds the
+            // non-empty line spans of an AccuTile set of at most kLaneRows lines (tmin | tmax << 9
+            // | line << 18), or up to kInlineEnt super-tile entries (super-tile | mask << 16), or
+            // -- for a Gaussian with more entries -- aux = t as float64 bits (AccuTile) or the
+            // packed rect (x0, x1-x0-1, y0, y1-y0-1) for the re-enumeration; info = span count |
+            // entries-inline 0x100 | columns 0x200 | AccuTile 0x400 | spans-inline 0x800 | entries << 12.
             uint32_t aux0, aux1;
             if (mode == SS_BIN_ACCUTILE) {
                 aux0 = (uint32_t)__double2loint(td);
@@ -310,8 +310,10 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
                                                : (n_ent <= (uint32_t)kInlineEnt ? kInfoEntInline : 0u)) |
                                   (cols ? kInfoCols : 0u) | (mode == SS_BIN_ACCUTILE ? kInfoAccuTile : 0u) |
                                   (n_ent << kInfoEntShift);
-            uint4 *er = erec + 4 * (size_t)i;
-            er[0] = make_uint4(count, info, aux0, aux1);
+            if (info & (kInfoSpanInline | kInfoEntInline))
+                *reinterpret_cast<uint2 *>(erec + 2 * (size_t)i) = make_uint2(count, info);
+            else
+                erec[2 * (size_t)i] = make_uint4(count, info, aux0, aux1);
             const uint32_t key = __float_as_uint(pz);
             depth_key[i] = key;
             gne[i] = n_ent;

@@ -100,8 +100,8 @@ class Rasterizer:
         return self._view(self.layout.rec, 12 * self.scene.n, torch.float32).view(self.scene.n, 12)
 
     def emit_records(self) -> torch.Tensor:
-        """[N, 16] int32 emission records: (count, info, aux0, aux1, entry0..11)."""
-        return self._view(self.layout.erec, 16 * self.scene.n, torch.int32).view(self.scene.n, 16)
+        """[N, 8] int32 emission records: (count, info, payload 0..5) (include/ss.h)."""
+        return self._view(self.layout.erec, 8 * self.scene.n, torch.int32).view(self.scene.n, 8)
 
     def counts(self) -> torch.Tensor:
         """Per-Gaussian tile count of the current frame (int32, 0 for Gaussians without tiles)."""

@@ -59,15 +59,28 @@ def _check_frame(scene, cam, mode, bg=(0.0, 0.0, 0.0), capacity=None, image=True
     assert np.array_equal(g["depth_key"][vis], orr[:, 2].view(np.uint32)), "depth keys"
     assert np.all(g["depth_key"][~vis] == 0xFFFFFFFF)
     er = g["erec"][vis]
+    big = (er[:, 1] & 0x900) == 0  # records holding aux (neither spans nor entries inline)
     if mode == "accutile":  # aux = t as float64 bits: 2 log(255 sigma) of the stored sigma
-        t64 = er[:, 2:4].copy().view(np.float64)[:, 0]
-        t_or = np.array([oracle.threshold(s) for s in orr[:, 6]])
+        t64 = er[big, 2:4].copy().view(np.float64)[:, 0]
+        t_or = np.array([oracle.threshold(s) for s in orr[big, 6]])
         assert np.all(np.abs(t64 - t_or) <= 4.5e-16 * np.abs(t_or))  # CUDA log vs glibc log (R2)
+        # line spans stored by the count = the oracle's AccuTile set, Gaussian by Gaussian
+        spn = np.nonzero((er[:, 1] & 0x800) != 0)[0][:300]
+        for j in spn:
+            gi = np.nonzero(vis)[0][j]
+            cols = (er[j, 1] & 0x200) != 0
+            tiles = set()
+            for w in er[j, 2:2 + (er[j, 1] & 0xFF)]:
+                lo, hi, line = w & 0x1FF, (w >> 9) & 0x1FF, w >> 18
+                for u in range(lo, hi):
+                    tiles.add(u * cam.tiles_x + line if cols else line * cam.tiles_x + u)
+            want = oracle.tiles_of_record(mode, f.rec[gi], f.rect[gi], cam.tiles_x, cam.tiles_y)
+            assert tiles == set(want.tolist()), f"spans of Gaussian {gi}"
     else:  # the packed tile rect
-        pr = er[:, 2]
+        pr = er[big, 2]
         x0, y0 = pr & 0xFF, (pr >> 16) & 0xFF
         rect = np.stack([x0, x0 + ((pr >> 8) & 0xFF) + 1, y0, y0 + (pr >> 24) + 1], 1)
-        assert np.array_equal(rect.astype(np.int32), f.rect[vis])
+        assert np.array_equal(rect.astype(np.int32), f.rect[vis][big])
     # depth order of the visible Gaussians: (depth bits, index) -- numpy's lexsort on the oracle records
     idx = np.nonzero(vis)[0]
     dbits = f.rec[idx, 2].view(np.uint32)
