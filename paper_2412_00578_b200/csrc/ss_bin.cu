@@ -629,9 +629,9 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_write(const uint32_t *__restr
                                                          const uint32_t *__restrict__ tile_base,
                                                          uint32_t *__restrict__ sorted_value) {
     pdl_enter();
-    __shared__ uint32_t s_bal[kL2Threads / 32][16];
-    __shared__ uint32_t s_off[kL2Threads / 32][16];
-    __shared__ uint32_t s_run[16];
+    constexpr int kW = kL2Threads / 32;
+    __shared__ uint32_t s_bal[kL2PerThread][kW][16];  // ballots of every (chunk, warp, tile)
+    __shared__ uint32_t s_off[kL2PerThread][kW][16];  // first position of every (chunk, warp, tile)
     if (*overflow || blockIdx.x >= *n_blocks) return;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -639,37 +639,39 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_write(const uint32_t *__restr
     const uint32_t n = min((uint32_t)kL2Block, st_total[bl.x] - bl.y);
     uint2 v[kL2PerThread];
     l2_load(ent, st_base[bl.x] + bl.y, n, v);
-    if (tid < 16)
-        s_run[tid] = tile_in_grid((int)bl.x, tid, stx, tiles_x, tiles_y)
-                         ? BC[(size_t)blockIdx.x * 16 + tid] + tile_base[tile_of((int)bl.x, tid, stx, tiles_x)]
-                         : 0u;
+    // all ballots of the block first (one barrier), then the per-tile prefixes over (chunk,
+    // warp) by 16 threads (one barrier), then every store
 #pragma unroll
     for (int q = 0; q < kL2PerThread; ++q) {
-        if ((uint32_t)q * kL2Threads >= n) break;
         const uint32_t m = v[q].y;
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
             const uint32_t bal = __ballot_sync(0xffffffffu, (m >> t) & 1u);
-            if (lane == t) s_bal[w][t] = bal;
+            if (lane == t) s_bal[q][w][t] = bal;
         }
-        __syncthreads();
-        if (tid < 16) {
-            uint32_t run = s_run[tid];
+    }
+    __syncthreads();
+    if (tid < 16) {
+        uint32_t run = tile_in_grid((int)bl.x, tid, stx, tiles_x, tiles_y)
+                           ? BC[(size_t)blockIdx.x * 16 + tid] + tile_base[tile_of((int)bl.x, tid, stx, tiles_x)]
+                           : 0u;
 #pragma unroll
-            for (int ww = 0; ww < kL2Threads / 32; ++ww) {
-                s_off[ww][tid] = run;
-                run += __popc(s_bal[ww][tid]);
+        for (int q = 0; q < kL2PerThread; ++q)
+#pragma unroll
+            for (int ww = 0; ww < kW; ++ww) {
+                s_off[q][ww][tid] = run;
+                run += __popc(s_bal[q][ww][tid]);
             }
-            s_run[tid] = run;
-        }
-        __syncthreads();
-        // tile by tile, so that each store instruction fills consecutive positions of one tile
+    }
+    __syncthreads();
 #pragma unroll
-        for (int t = 0; t < 16; ++t) {
-            const uint32_t bal = s_bal[w][t];
-            if ((m >> t) & 1u) sorted_value[s_off[w][t] + __popc(bal & lt_mask)] = v[q].x;
+    for (int q = 0; q < kL2PerThread; ++q) {
+        uint32_t m = v[q].y;
+        while (m) {  // the entry's tiles (2.3 on average)
+            const int t = __ffs(m) - 1;
+            m &= m - 1;
+            sorted_value[s_off[q][w][t] + __popc(s_bal[q][w][t] & lt_mask)] = v[q].x;
         }
-        __syncthreads();
     }
 }
 
