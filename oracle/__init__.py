@@ -16,6 +16,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "ss_oracle.c")
+_SRC_BWD = os.path.join(_HERE, "ss_oracle_bwd.c")  # render / preprocess backward (NEXT-2)
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}
@@ -27,8 +28,10 @@ GCC_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11", "-Wall", 
 
 def build(force: bool = False) -> str:
     """Compile liboracle.so (plain C; the checker, not the product)."""
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", *GCC_FLAGS, "-o", _LIB_PATH, _SRC, "-lm"])
+    srcs = [_SRC, _SRC_BWD]
+    if force or not os.path.exists(_LIB_PATH) or \
+            os.path.getmtime(_LIB_PATH) < max(os.path.getmtime(f) for f in srcs):
+        subprocess.check_call(["gcc", *GCC_FLAGS, "-o", _LIB_PATH, *srcs, "-lm"])
     return _LIB_PATH
 
 
@@ -68,6 +71,11 @@ def lib():
             "or_render_tiles": (None, [vp, vp, vp, i, i, vp, vp, i, vp, vp, vp]),
             "or_prune_score_tiles": (None, [vp, vp, vp, i, i, vp, vp, vp, i]),
             "or_prune_select": (C.c_int64, [i, vp, d, vp]),
+            "or_project_f64": (None, [i, i, vp, vp, vp, vp, vp, vp]),
+            "or_loss_f64": (d, [i, vp, i, i, vp, vp, i, i, i, i, vp]),
+            "or_render_backward": (None, [vp, vp, vp, i, i, vp, vp, i, i, i, i, vp, vp]),
+            "or_render_backward_tiles": (None, [vp, vp, vp, i, i, vp, vp, vp, i, vp, vp]),
+            "or_project_backward": (None, [i, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "or_frame": (u64, [i, i, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp, vp, vp, u64, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
@@ -298,3 +306,68 @@ def prune_select(score: np.ndarray, ratio: float):
     keep = np.zeros(len(score), np.uint8)
     k = lib().or_prune_select(len(score), _p(score), float(ratio), _p(keep))
     return keep, int(k)
+
+
+# ---- backward (ss_oracle_bwd.c) ----------------------------------------
+G_FIELDS = ["x", "y", "a", "b", "c", "sigma", "r", "g", "b_"]   # g2d columns
+F_NF = 11                                                        # or_project_f64 record width
+
+
+def project_f64(scene, cam) -> np.ndarray:
+    """float64 projection (parameters read as float64; scene arrays may be float64) rec64[n][11] = (x2d, y2d, depth, a, b, c, sigma, r, g, b, visible)."""
+    out = np.zeros((scene.n, F_NF), np.float64)
+    mo, sc, ro, sh = (np.ascontiguousarray(a, np.float64) for a in (scene.mean_opac, scene.scale, scene.rot, scene.sh))
+    lib().or_project_f64(scene.n, scene.sh_degree, _p(mo), _p(sc), _p(ro), _p(sh), C.byref(camera(cam)), _p(out))
+    return out
+
+
+def loss_f64(rec64, width, height, weights, bg=(0.0, 0.0, 0.0), window=None, with_hash=False):
+    """L = sum w * C of the float64 unbinned render of rec64 (weights float64 [3][H][W]);
+    with_hash: also the hash of the blended (pixel, Gaussian) set."""
+    rec64 = np.ascontiguousarray(rec64, np.float64)
+    w = np.ascontiguousarray(weights, np.float64)
+    x0, x1, y0, y1 = window if window else (0, width, 0, height)
+    h = C.c_uint64(0)
+    L = lib().or_loss_f64(len(rec64), _p(rec64), width, height, _p(np.asarray(bg, np.float64)), _p(w),
+                          x0, x1, y0, y1, C.byref(h))
+    return (L, h.value) if with_hash else L
+
+
+def render_backward(rec, values, ranges, width, height, dimg, bg=(0.0, 0.0, 0.0), window=None,
+                    tiles=None, g2d=None, gabs=None):
+    """dL/d(x2d, y2d, a, b, c, sigma, r, g, b) per Gaussian (float64 [n][9], accumulated) and
+    the sums of absolute per-pixel terms (same shape).  dimg = dL/dC float32 [3][H][W]."""
+    rec = np.ascontiguousarray(rec, np.float32)
+    n = len(rec)
+    if g2d is None:
+        g2d = np.zeros((n, 9), np.float64)
+    if gabs is None:
+        gabs = np.zeros((n, 9), np.float64)
+    dimg = np.ascontiguousarray(dimg, np.float32)
+    bgv = np.asarray(bg, np.float32)
+    v = np.ascontiguousarray(values, np.uint32)
+    r = np.ascontiguousarray(ranges, np.uint32)
+    if tiles is not None:
+        tl = np.ascontiguousarray(tiles, np.int32)
+        lib().or_render_backward_tiles(_p(rec), _p(v), _p(r), width, height, _p(bgv), _p(dimg), _p(tl), len(tl),
+                                       _p(g2d), _p(gabs))
+    else:
+        x0, x1, y0, y1 = window if window else (0, width, 0, height)
+        lib().or_render_backward(_p(rec), _p(v), _p(r), width, height, _p(bgv), _p(dimg), x0, x1, y0, y1,
+                                 _p(g2d), _p(gabs))
+    return g2d, gabs
+
+
+def project_backward(scene, cam, g2d):
+    """Accumulated float64 parameter gradients (dmean_opac [n][4], dscale [n][4], drot [n][4],
+    dsh like scene.sh) from g2d float64 [n][9]."""
+    n = scene.n
+    dmo = np.zeros((n, 4), np.float64)
+    ds = np.zeros((n, 4), np.float64)
+    dr = np.zeros((n, 4), np.float64)
+    dsh = np.zeros(scene.sh.shape, np.float64)
+    g2d = np.ascontiguousarray(g2d, np.float64)
+    mo, sc, ro, sh = (np.ascontiguousarray(a, np.float64) for a in (scene.mean_opac, scene.scale, scene.rot, scene.sh))
+    lib().or_project_backward(n, scene.sh_degree, _p(mo), _p(sc), _p(ro), _p(sh), C.byref(camera(cam)), _p(g2d),
+                              _p(dmo), _p(ds), _p(dr), _p(dsh))
+    return dmo, ds, dr, dsh

@@ -291,3 +291,38 @@ def random_conics(n, seed, tiles=40, cond_max=1e3, sigma_range=(1.0 / 255.0 + 1e
     my = rng.uniform(-20, tiles * 16 + 20, n)
     sig = rng.uniform(sigma_range[0], sigma_range[1], n)
     return mx, my, cxx, cxy, cyy, sig
+
+
+def grad_scene(n=40, width=72, height=40, seed=7, opac=(0.05, 0.5), px_sigma=(1.0, 6.0), sh_degree=3,
+               margin=8.0, yaw_deg=0.0) -> tuple[Scene, Camera]:
+    """Small scene for the backward pins and parity tests: `n` Gaussians in
+    front of a width x height camera (ragged tiles when the sides are not multiples of 16),
+    means uniform in pixel space (-margin .. side+margin) at depth z in [2, 6], projected
+    1-sigma extents log-uniform in `px_sigma`, opacity uniform in `opac` (the default upper
+    bound keeps transmittance far from the 1e-4 stop), Haar quaternions, SH as the tiny
+    scene.  `yaw_deg` turns the camera so the world->camera rotation is not the identity."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    cam0 = look_at((0, 0, 0), (0, 0, 1), width, height, 60.0, up=(0, -1, 0))
+    u = rng.uniform(-margin, width + margin, n)
+    v = rng.uniform(-margin, height + margin, n)
+    z = rng.uniform(2.0, 6.0, n)
+    x = (u - cam0.cx) * z / cam0.fx
+    y = (v - cam0.cy) * z / cam0.fy
+    pxs = np.exp(rng.uniform(math.log(px_sigma[0]), math.log(px_sigma[1]), (n, 3)))
+    scale = pxs * z[:, None] / cam0.fx
+    o = rng.uniform(opac[0], opac[1], n)
+    p_cam = np.stack([x, y, z], 1)
+    if yaw_deg:
+        a = math.radians(yaw_deg)
+        pos = np.array([0.3, -0.2, 0.1])
+        fwd = np.array([math.sin(a), 0.0, math.cos(a)])
+        cam = look_at(pos, pos + fwd, width, height, 60.0, up=(0, -1, 0))
+        Rm = cam.viewmat[:, :3].astype(np.float64)
+        world = (p_cam - cam.viewmat[:, 3].astype(np.float64)) @ Rm  # R^T (p - t)
+    else:
+        cam, world = cam0, p_cam
+    mean_opac = np.concatenate([world, o[:, None]], 1).astype(np.float32)
+    sc = np.concatenate([scale, np.zeros((n, 1))], 1).astype(np.float32)
+    q = rng.standard_normal((n, 4))
+    q *= rng.uniform(0.5, 2.0, (n, 1)) / np.linalg.norm(q, axis=1, keepdims=True)  # non-unit: normalised in-kernel
+    return Scene(mean_opac, sc, q.astype(np.float32), _sh_planes(rng, n, sh_degree), sh_degree, "grad"), cam
