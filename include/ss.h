@@ -207,6 +207,40 @@ SS_API ss_status ss_prune_select(const double *score, int32_t n, double ratio, u
 SS_API ss_status ss_compact_scene(const ss_scene *in /*host*/, const uint8_t *keep, const ss_scene *out /*host*/,
                                   uint32_t *n_out, void *ws, size_t ws_bytes, void *stream);
 
+/* ---- NEXT-2: backward of the forward path ("the per-pixel gradients from the render
+ * kernel are parallelized and aggregated to the 2D mu_2D and Sigma_2D parameters, which are
+ * then parallelized across Gaussians to compute gradients for mu and s").  The gradient is
+ * the derivative of the forward above where it is differentiable (reading R25):
+ * a clamped alpha (0.99), a clamped J entry and a clamped colour pass nothing through the
+ * clamped quantity; t, the tile sets and the depth order carry no gradient.
+ *
+ * ss_render_backward: for the frame of the last ss_sort (records, sorted values, ranges in the
+ * workspace) and its ss_render outputs T_final (float32 [H][W]) and n_contrib (uint32 [H][W]),
+ * given dL_dimg = dL/dC (float32 [3][H][W], planar like out_rgb) and the same bg, ACCUMULATES
+ * into grad2d (float32 [n][12], caller-zeroed once) per Gaussian:
+ *   (dL/dx2d, dL/dy2d, dL/da, dL/db | dL/dc, dL/dsigma, dL/dr, dL/dg | dL/db_rgb, 0, 0, 0)
+ * with (a, b, c) the conic of the record (q = a dx^2 + 2 b dx dy + c dy^2) and (x2d, y2d) the
+ * projected mean (its magnitude is 3D-GS's densification signal).  Per tile, back to front
+ * from each pixel's last blended entry; float32 atomics (summation order is not fixed). */
+SS_API ss_status ss_render_backward(const ss_frame *frame /*host*/, const float *bg /*host [3]*/,
+                                    const float *dL_dimg, const float *T_final, const uint32_t *n_contrib,
+                                    float *grad2d, void *stream);
+
+/* Gradient arrays laid out exactly like ss_scene's (mean_opac: dL/d(x, y, z, sigma); scale:
+ * dL/d(sx, sy, sz), w untouched; rot: dL/d(w, x, y, z) of the UNNORMALISED quaternion; sh:
+ * per-Gaussian blocks like scene->sh). */
+typedef struct {
+    int32_t n, sh_degree;
+    float *mean_opac, *scale, *rot, *sh;
+} ss_scene_grad;
+
+/* ss_preprocess_backward: chain rule of ss_preprocess (Eqs. 3-4, 10, SH colour) from grad2d of
+ * one view to the scene parameters, ACCUMULATED (+=) into `grad` (so views can be summed; the
+ * caller zeroes it).  One thread per Gaussian; Gaussians with an all-zero grad2d row are
+ * skipped.  grad->n and grad->sh_degree must equal the scene's. */
+SS_API ss_status ss_preprocess_backward(const ss_scene *scene /*host*/, const ss_camera *cam /*host*/,
+                                        const float *grad2d, const ss_scene_grad *grad /*host*/, void *stream);
+
 /* Convenience: ss_preprocess + ss_bin + ss_sort + ss_render in one call. */
 SS_API ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
                           const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib, void *stream);

@@ -14,7 +14,8 @@ MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}
 
 EXPORTS = ["ss_frame_workspace_size", "ss_frame_layout", "ss_preprocess", "ss_bin", "ss_sort", "ss_sorted_keys",
            "ss_render", "ss_render_stats", "ss_prune_score", "ss_render_frame",
-           "ss_prune_workspace_size", "ss_prune_count", "ss_prune_select", "ss_compact_scene", "ss_status_string", "ss_last_cuda_error", "ss_version"]
+           "ss_prune_workspace_size", "ss_prune_count", "ss_prune_select", "ss_compact_scene",
+           "ss_render_backward", "ss_preprocess_backward", "ss_status_string", "ss_last_cuda_error", "ss_version"]
 
 
 class SsScene(C.Structure):
@@ -69,6 +70,8 @@ def lib() -> C.CDLL:
             "ss_prune_count": (C.c_uint32, [C.c_int32, C.c_double]),
             "ss_prune_select": (st, [vp, C.c_int32, C.c_double, vp, vp, C.c_size_t, vp]),
             "ss_compact_scene": (st, [P(SsScene), vp, P(SsScene), vp, vp, C.c_size_t, vp]),
+            "ss_render_backward": (st, [P(SsFrame), P(C.c_float), vp, vp, vp, vp, vp]),
+            "ss_preprocess_backward": (st, [P(SsScene), P(SsCamera), vp, P(SsScene), vp]),
             "ss_status_string": (C.c_char_p, [st]),
             "ss_last_cuda_error": (C.c_char_p, []),
             "ss_version": (C.c_char_p, []),

@@ -27,6 +27,7 @@ UNITS = {
     "ss_sort.cu": [],
     "ss_render.cu": [],
     "ss_prune.cu": [],
+    "ss_backward.cu": [],
 }
 HEADERS = ["ss_common.cuh", "ss_tilegeom.cuh"]
 

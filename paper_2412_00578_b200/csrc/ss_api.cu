@@ -213,6 +213,31 @@ ss_status ss_prune_score(const ss_frame *frame, const float *bg, double *score, 
                                           static_cast<cudaStream_t>(stream)));
 }
 
+ss_status ss_render_backward(const ss_frame *frame, const float *bg, const float *dL_dimg, const float *T_final,
+                             const uint32_t *n_contrib, float *grad2d, void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    if (!bg || !dL_dimg || !T_final || !n_contrib || (!grad2d && frame->n > 0)) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_render_backward(frame->ws, L, frame->width, frame->height, bg[0], bg[1], bg[2], dL_dimg,
+                                              T_final, n_contrib, grad2d, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_preprocess_backward(const ss_scene *scene, const ss_camera *cam, const float *grad2d,
+                                 const ss_scene_grad *grad, void *stream) {
+    if (!scene || !cam || !grad || scene->n < 0 || scene->sh_degree < 0 || scene->sh_degree > 3) return SS_ERR_INVALID_ARG;
+    if (grad->n != scene->n || grad->sh_degree != scene->sh_degree) return SS_ERR_INVALID_ARG;
+    if (scene->n >= (1 << 30)) return SS_ERR_UNSUPPORTED;
+    if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0.0f) || !(cam->fy > 0.0f)) return SS_ERR_INVALID_ARG;
+    if (scene->n > 0 && (!scene->mean_opac || !scene->scale || !scene->rot || !scene->sh || !grad2d ||
+                         !grad->mean_opac || !grad->scale || !grad->rot || !grad->sh))
+        return SS_ERR_INVALID_ARG;
+    Layout L;
+    if (!compute_layout(scene->n, 0, cam->width, cam->height, &L)) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_preprocess_backward(*scene, cam_args(*cam, L), grad2d, *grad,
+                                                  static_cast<cudaStream_t>(stream)));
+}
+
 ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
                           const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib, void *stream) {
     ss_status s = ss_preprocess(scene, cam, mode, frame, stream);

@@ -146,6 +146,11 @@ cudaError_t launch_render_stats(void *ws, const Layout &L, int W, int H, unsigne
                                 cudaStream_t st);
 cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2,
                                double *score, cudaStream_t st);
+cudaError_t launch_render_backward(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2,
+                                   const float *dimg, const float *T_final, const uint32_t *n_contrib, float *grad2d,
+                                   cudaStream_t st);
+cudaError_t launch_preprocess_backward(const ss_scene &sc, const CamArgs &cam, const float *grad2d,
+                                       const ss_scene_grad &out, cudaStream_t st);
 
 size_t prune_workspace_bytes(int32_t n);
 cudaError_t launch_prune_select(const double *score, int32_t n, double ratio, uint8_t *keep, void *ws,

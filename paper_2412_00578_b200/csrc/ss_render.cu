@@ -1,4 +1,5 @@
-// ss_render.cu -- a6 render (Eqs. 5-7) and a7 efficient pruning score (Eqs. 20-21).
+// ss_render.cu -- a6 render (Eqs. 5-7), a7 efficient pruning score (Eqs. 20-21) and the
+// NEXT-2 render backward.
 //
 // One CTA per 16x16 tile, one thread per pixel ("parallelized across pixels").  The
 // tile's depth-ordered Gaussian ids are consumed in batches of 256: each thread gathers one
@@ -300,6 +301,156 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
     }
 }
 
+// NEXT-2 render backward ("the per-pixel gradients from the render kernel are
+// parallelized and aggregated to the 2D mu_2D and Sigma_2D parameters").  One CTA per tile,
+// one thread per pixel, walking the tile list back to front from the pixel's last blended
+// entry (n_contrib of ss_render) with T recovered as T_i = T_{i+1} / (1 - alpha_i) and the
+// suffix colour S <- alpha c + (1 - alpha) S (a7's recursion):
+//   dL/dalpha_i = sum_ch dL/dC_ch (T_i (c_ch - S_ch) - T_final bg_ch / (1 - alpha_i))
+//   dL/dc_i     = dL/dC alpha_i T_i
+//   unclamped alpha = sigma G:  dL/dsigma = dL/dalpha G,  dL/dq = -dL/dalpha alpha / 2,
+//   dq/dx2d = -2 (a dx + b dy), dq/dy2d = -2 (b dx + c dy), dq/d(a, b, c) = (dx^2, 2 dx dy, dy^2)
+// (a clamped alpha passes nothing to sigma and the geometry, reading R25).  The alpha of
+// every entry is recomputed with k_render's exact operations, so the blended set is the
+// forward's.  Per batch, each warp reduces a Gaussian's 9 partials by shuffles (only when
+// one of its pixels contributes) into shared-memory accumulators; the CTA then adds each
+// Gaussian's sums to grad2d with three float4 atomics (one set per (tile, Gaussian)).
+__global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict__ ranges,
+                                                         const uint32_t *__restrict__ vals,
+                                                         const float4 *__restrict__ rec, int W, int H, int tiles_x,
+                                                         float bg0, float bg1, float bg2,
+                                                         const float *__restrict__ dimg,
+                                                         const float *__restrict__ T_final,
+                                                         const uint32_t *__restrict__ n_contrib,
+                                                         float4 *__restrict__ grad2d) {
+    pdl_enter();
+    __shared__ Batch s;
+    __shared__ PixState st;  // T (running), C0..2 = suffix S, last = n_contrib
+    __shared__ float s_dC[3][256];
+    __shared__ float s_Tfin[256];
+    __shared__ uint32_t s_id[kBatch];
+    __shared__ float s_acc[9][kBatch];
+    __shared__ uint32_t s_warp[8];
+    __shared__ uint32_t s_max;
+    const int tile = blockIdx.x;
+    int mpx, mpy;
+    tile_pixel(tile, tiles_x, threadIdx.x, mpx, mpy);
+    const bool inside = mpx < W && mpy < H;
+    const uint2 range = ranges[tile];
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) s_max = 0;
+    const size_t pix = (size_t)mpy * W + mpx, plane = (size_t)W * H;
+    const uint32_t my_last = inside ? n_contrib[pix] : 0u;
+    st.last[threadIdx.x] = my_last;
+    st.T[threadIdx.x] = s_Tfin[threadIdx.x] = inside ? T_final[pix] : 1.0f;
+    st.C0[threadIdx.x] = st.C1[threadIdx.x] = st.C2[threadIdx.x] = 0.0f;
+    s_dC[0][threadIdx.x] = inside ? dimg[pix] : 0.0f;
+    s_dC[1][threadIdx.x] = inside ? dimg[plane + pix] : 0.0f;
+    s_dC[2][threadIdx.x] = inside ? dimg[2 * plane + pix] : 0.0f;
+    for (int k = threadIdx.x; k < 9 * kBatch; k += 256) (&s_acc[0][0])[k] = 0.0f;
+    __syncthreads();
+    if (my_last) atomicMax(&s_max, my_last);
+    __syncthreads();
+    const uint32_t max_last = min(s_max, range.y - range.x);
+    for (uint32_t end = range.x + max_last; end > range.x;) {
+        const uint32_t start = end - range.x > (uint32_t)kBatch ? end - kBatch : range.x;
+        const int cnt = (int)(end - start);
+        __syncthreads();
+        const uint32_t n_active = compact_active(my_last > start - range.x, st, s_warp);
+        load_batch(s, vals, rec, start + threadIdx.x, end, s_id);
+        __syncthreads();
+        const uint32_t n_warps = (n_active + 31) / 32;
+        if ((uint32_t)(threadIdx.x >> 5) < n_warps) {
+            const bool act = threadIdx.x < n_active;
+            const int pp = act ? st.list[threadIdx.x] : 0;
+            int px, py;
+            tile_pixel(tile, tiles_x, pp, px, py);
+            const float fpx = (float)px, fpy = (float)py;
+            const uint32_t plast = act ? st.last[pp] : 0u;
+            const float Tfin = s_Tfin[pp];
+            const float dC0 = s_dC[0][pp], dC1 = s_dC[1][pp], dC2 = s_dC[2][pp];
+            float T = st.T[pp];
+            float S0 = st.C0[pp], S1 = st.C1[pp], S2 = st.C2[pp];
+            for (int k = cnt - 1; k >= 0; --k) {
+                float g[9];
+#pragma unroll
+                for (int f = 0; f < 9; ++f) g[f] = 0.0f;
+                bool any = false;
+                if (start - range.x + (uint32_t)k < plast) {
+                    const float4 bx = s.box[k];
+                    const float4 cn = s.con[k];
+                    const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
+                    if (q <= cn.w) {
+                        const float4 cl = s.col[k];
+                        float e;
+                        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(q * -0.72134752044448170f));
+                        const float raw = cl.w * e;
+                        const float alpha = fminf(0.99f, raw);  // == alpha_of(q, sigma)
+                        const float om = 1.0f - alpha;
+                        T = T / om;
+                        const float bgs = Tfin / om;
+                        const float dLda = dC0 * (T * (cl.x - S0) - bgs * bg0) + dC1 * (T * (cl.y - S1) - bgs * bg1) +
+                                           dC2 * (T * (cl.z - S2) - bgs * bg2);
+                        const float w = alpha * T;
+                        g[6] = dC0 * w;
+                        g[7] = dC1 * w;
+                        g[8] = dC2 * w;
+                        if (raw <= 0.99f) {
+                            const float dx = fpx - bx.x, dy = fpy - bx.y;
+                            const float b = 0.5f * cn.y;
+                            const float dLdq = -0.5f * dLda * alpha;
+                            g[0] = -2.0f * dLdq * (cn.x * dx + b * dy);
+                            g[1] = -2.0f * dLdq * (b * dx + cn.z * dy);
+                            g[2] = dLdq * dx * dx;
+                            g[3] = 2.0f * dLdq * dx * dy;
+                            g[4] = dLdq * dy * dy;
+                            g[5] = dLda * e;
+                        }
+                        S0 = alpha * cl.x + om * S0;
+                        S1 = alpha * cl.y + om * S1;
+                        S2 = alpha * cl.z + om * S2;
+                        any = true;
+                    }
+                }
+                if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+                    for (int f = 0; f < 9; ++f) {
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) g[f] += __shfl_xor_sync(0xffffffffu, g[f], o);
+                    }
+                    if (lane == 0) {
+#pragma unroll
+                        for (int f = 0; f < 9; ++f) atomicAdd(&s_acc[f][k], g[f]);
+                    }
+                }
+            }
+            if (act) {
+                st.T[pp] = T;
+                st.C0[pp] = S0;
+                st.C1[pp] = S1;
+                st.C2[pp] = S2;
+            }
+        }
+        __syncthreads();
+        if ((int)threadIdx.x < cnt) {
+            const int k = threadIdx.x;
+            const float4 a0 = make_float4(s_acc[0][k], s_acc[1][k], s_acc[2][k], s_acc[3][k]);
+            const float4 a1 = make_float4(s_acc[4][k], s_acc[5][k], s_acc[6][k], s_acc[7][k]);
+            const float a2 = s_acc[8][k];
+#pragma unroll
+            for (int f = 0; f < 9; ++f) s_acc[f][k] = 0.0f;
+            if (a0.x != 0.f || a0.y != 0.f || a0.z != 0.f || a0.w != 0.f || a1.x != 0.f || a1.y != 0.f ||
+                a1.z != 0.f || a1.w != 0.f || a2 != 0.f) {
+                float4 *gp = grad2d + 3 * (size_t)s_id[k];
+                atomicAdd(gp + 0, a0);
+                atomicAdd(gp + 1, a1);
+                atomicAdd(&gp[2].x, a2);
+            }
+        }
+        end = start;
+    }
+}
+
 // Measurement only (not on the timed path): the render's work counts for one frame, from
 // the same per-pixel walk as k_render.  counters[0] += E_pix (evaluations each pixel makes
 // until it terminates, the method's work), [1] += E_blend (evaluations that blend),
@@ -388,6 +539,17 @@ cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, fl
         launch_pdl(k_render<false>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
                                                     at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
                                                     out_T, out_nc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_render_backward(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2,
+                                   const float *dimg, const float *T_final, const uint32_t *n_contrib, float *grad2d,
+                                   cudaStream_t st) {
+    const ss_layout &P = L.pub;
+    if (P.n_tiles == 0) return cudaSuccess;
+    launch_pdl(k_render_backward, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges),
+               at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
+               dimg, T_final, n_contrib, reinterpret_cast<float4 *>(grad2d));
     return cudaGetLastError();
 }
 

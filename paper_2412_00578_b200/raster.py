@@ -45,6 +45,15 @@ class DeviceScene:
         return SsScene(self.n, self.sh_degree, self.mean_opac.data_ptr(), self.scale.data_ptr(),
                        self.rot.data_ptr(), self.sh.data_ptr())
 
+    def zeros_like(self) -> "DeviceScene":
+        """Gradient arrays with the scene's layout (ss_scene_grad), zero-filled."""
+        z = torch.zeros_like
+        return DeviceScene(z(self.mean_opac), z(self.scale), z(self.rot), z(self.sh), self.sh_degree)
+
+    def host_sh_planes(self) -> np.ndarray:
+        """SH in the host layout [B][N][4] (the inverse of from_host's transpose)."""
+        return np.ascontiguousarray(np.transpose(self.sh.cpu().numpy(), (1, 0, 2)))
+
 
 def camera_struct(cam) -> SsCamera:
     if isinstance(cam, SsCamera):
@@ -179,6 +188,44 @@ class Rasterizer:
         check(lib().ss_prune_score(C.byref(self.frame), bgv, C.c_void_p(score.data_ptr()),
                                    C.c_void_p(_stream_handle(stream))), "ss_prune_score")
         return score
+
+    # ---------------------------------------------------------------- backward (NEXT-2)
+    def render_backward(self, dL_dimg: torch.Tensor, T_final: torch.Tensor, n_contrib: torch.Tensor,
+                        grad2d: torch.Tensor | None = None, bg=(0.0, 0.0, 0.0), stream=None) -> torch.Tensor:
+        """grad2d [N, 12] float32 += dL/d(x2d, y2d, a, b | c, sigma, r, g | b, -, -, -) of the
+        current frame, from dL/dC (float32 [3, H, W]) and the T_final / n_contrib of its render."""
+        if grad2d is None:
+            grad2d = torch.zeros((self.scene.n, 12), dtype=torch.float32, device=self.device)
+        for t, shape in ((dL_dimg, (3, self.height, self.width)), (T_final, (self.height, self.width)),
+                         (n_contrib, (self.height, self.width))):
+            assert tuple(t.shape) == shape and t.is_cuda and t.is_contiguous()
+        assert grad2d.dtype == torch.float32 and grad2d.shape == (self.scene.n, 12) and grad2d.is_contiguous()
+        bgv = (C.c_float * 3)(*[float(v) for v in bg])
+        check(lib().ss_render_backward(C.byref(self.frame), bgv, C.c_void_p(dL_dimg.data_ptr()),
+                                       C.c_void_p(T_final.data_ptr()), C.c_void_p(n_contrib.data_ptr()),
+                                       C.c_void_p(grad2d.data_ptr()), C.c_void_p(_stream_handle(stream))),
+              "ss_render_backward")
+        return grad2d
+
+    def preprocess_backward(self, cam, grad2d: torch.Tensor, grads: DeviceScene | None = None,
+                            stream=None) -> DeviceScene:
+        """Scene-parameter gradients += chain rule of ss_preprocess applied to grad2d."""
+        if grads is None:
+            grads = self.scene.zeros_like()
+        g = grads.struct()
+        c = camera_struct(cam)
+        check(lib().ss_preprocess_backward(C.byref(self._scene_struct), C.byref(c), C.c_void_p(grad2d.data_ptr()),
+                                           C.byref(g), C.c_void_p(_stream_handle(stream))), "ss_preprocess_backward")
+        return grads
+
+    def forward_backward(self, cam, dL_dimg_fn, bg=(0.0, 0.0, 0.0), grads: DeviceScene | None = None,
+                         stream=None):
+        """One training-style step for a view: render, dL/dC = dL_dimg_fn(image), render
+        backward, preprocess backward.  Returns (image, grads, grad2d)."""
+        img, T, nc = self.render_frame(cam, bg, want_T=True, want_ncontrib=True, stream=stream)
+        grad2d = self.render_backward(dL_dimg_fn(img), T, nc, bg=bg, stream=stream)
+        grads = self.preprocess_backward(cam, grad2d, grads, stream=stream)
+        return img, grads, grad2d
 
     # ---------------------------------------------------------------- conveniences
     def prepare(self, cam, stream=None) -> None:
