@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-score", action="store_true")
+    ap.add_argument("--no-backward", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for profilers: no clocks/e2e/cpu legs")
     return ap.parse_args()
 
@@ -363,6 +364,65 @@ def run_ours(args):
                       "ms_score_views": a.elapsed_time(b), "ms_allreduce": b.elapsed_time(c),
                       "allreduce_bytes": 8 * ds.n, "dtype": "f64 accumulate, f32 per-pixel"}
 
+    # ---- backward pass (NEXT-2): forward with T / n_contrib, render backward, preprocess backward
+    bw_info = None
+    if not args.no_backward:
+        n_bw = min(len(my_views), V if not args.ncu else 2)
+        grad2d = torch.zeros((ds.n, 12), dtype=torch.float32, device=dev)
+        grads = ds.zeros_like()
+        dimg = torch.empty((3, H, W), dtype=torch.float32, device=dev).uniform_(-1.0, 1.0)
+        bev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(n_bw)]
+
+        def fwd_bwd(v, e=None):
+            if e is not None:
+                e[0].record(stream)
+            rz.prepare(cstructs[v])
+            _, T_, nc_ = rz.render(out=out, want_T=True, want_ncontrib=True)
+            if e is not None:
+                e[1].record(stream)
+            grad2d.zero_()
+            if e is not None:
+                e[2].record(stream)
+            rz.render_backward(dimg, T_, nc_, grad2d=grad2d)
+            if e is not None:
+                e[3].record(stream)
+            rz.preprocess_backward(cstructs[v], grad2d, grads)
+            if e is not None:
+                e[4].record(stream)
+
+        for v in my_views[:4]:
+            fwd_bwd(v)
+        dist.barrier()
+        torch.cuda.synchronize()
+        flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for j, v in enumerate(my_views[:n_bw]):
+            fwd_bwd(v, bev[j])
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms_b = dist.max_over_ranks(a.elapsed_time(b))
+        rb_ms = sum(e[2].elapsed_time(e[3]) for e in bev) / n_bw
+        pb_ms = sum(e[3].elapsed_time(e[4]) for e in bev) / n_bw
+        Pb = float(np.mean([pairs[v] for v in my_views[:n_bw]]))
+        NVb = float(np.mean([nvis[v] for v in my_views[:n_bw]]))
+        # algorithmic bytes: render backward reads id + record per pair, dL/dC + T + n_contrib per
+        # pixel, and adds 36 B of gradient per (tile, Gaussian) pair; preprocess backward reads the
+        # 48 B grad2d row of every Gaussian, and per visible one its parameters (48 B + SH) and
+        # read-modify-writes its gradients (48 B + SH)
+        rb_bytes = 40 * Pb + 20 * W * H + 2 * 36 * Pb
+        pb_bytes = 48 * ds.n + NVb * (48 + 4 * sh_floats) + 2 * NVb * (48 + 4 * sh_floats)
+        bw_info = {"views_per_s": world * n_bw / (ms_b / 1e3), "views": world * n_bw,
+                   "note": "per view: a1-a6 with T_final / n_contrib, grad2d zeroing, ss_render_backward, "
+                           "ss_preprocess_backward (dL/dC uniform random, resident)",
+                   "render_backward": {"ms": rb_ms, "bound": "hbm", "bytes": rb_bytes,
+                                       "achieved": rb_bytes / (rb_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                                       "frac": rb_bytes / (rb_ms / 1e3) / 1e9 / hbm_peak},
+                   "preprocess_backward": {"ms": pb_ms, "bound": "hbm", "bytes": pb_bytes,
+                                           "achieved": pb_bytes / (pb_ms / 1e3) / 1e9, "peak": hbm_peak,
+                                           "unit": "GB/s", "frac": pb_bytes / (pb_ms / 1e3) / 1e9 / hbm_peak}}
+        del grad2d, grads
+
     # ---- end to end through the public API: camera in, image out to pinned host memory
     e2e = None
     if not args.no_e2e and not args.ncu:
@@ -419,6 +479,7 @@ def run_ours(args):
             "clocks": clk,
             "e2e": e2e,
             "prune_score": score_info,
+            "backward": bw_info,
             "cpu_baseline": cpu,
             "paper_context": {"gpu": "RTX A5000 (PAPER.md P:447)", "accutile_fps_avg_scene": 267,
                               "speedups": {"snugbox": 1.82, "accutile": 1.99, "overall": 6.71}},

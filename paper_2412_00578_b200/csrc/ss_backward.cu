@@ -53,7 +53,7 @@ __device__ __forceinline__ void sh_basis_grad(float x, float y, float z, float *
 }
 
 template <int DEG>
-__global__ void __launch_bounds__(256) k_preprocess_backward(int n, const float4 *__restrict__ mean_opac,
+__global__ void __launch_bounds__(256, 2) k_preprocess_backward(int n, const float4 *__restrict__ mean_opac,
                                                              const float4 *__restrict__ scale,
                                                              const float4 *__restrict__ rot,
                                                              const float4 *__restrict__ sh, CamArgs cam,

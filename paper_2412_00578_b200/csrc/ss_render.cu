@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
     __shared__ float s_dC[3][256];
     __shared__ float s_Tfin[256];
     __shared__ uint32_t s_id[kBatch];
-    __shared__ float s_acc[9][kBatch];
+    __shared__ float s_acc[9][kBatch + 1];  // +1: the 8 field rows in distinct banks
     __shared__ uint32_t s_warp[8];
     __shared__ uint32_t s_max;
     const int tile = blockIdx.x;
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
     s_dC[0][threadIdx.x] = inside ? dimg[pix] : 0.0f;
     s_dC[1][threadIdx.x] = inside ? dimg[plane + pix] : 0.0f;
     s_dC[2][threadIdx.x] = inside ? dimg[2 * plane + pix] : 0.0f;
-    for (int k = threadIdx.x; k < 9 * kBatch; k += 256) (&s_acc[0][0])[k] = 0.0f;
+    for (int k = threadIdx.x; k < 9 * (kBatch + 1); k += 256) (&s_acc[0][0])[k] = 0.0f;
     __syncthreads();
     if (my_last) atomicMax(&s_max, my_last);
     __syncthreads();
@@ -387,8 +387,9 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
                         const float raw = cl.w * e;
                         const float alpha = fminf(0.99f, raw);  // == alpha_of(q, sigma)
                         const float om = 1.0f - alpha;
-                        T = T / om;
-                        const float bgs = Tfin / om;
+                        const float rom = __frcp_rn(om);  // T_i = T_{i+1} / (1 - alpha_i)
+                        T = T * rom;
+                        const float bgs = Tfin * rom;
                         const float dLda = dC0 * (T * (cl.x - S0) - bgs * bg0) + dC1 * (T * (cl.y - S1) - bgs * bg1) +
                                            dC2 * (T * (cl.z - S2) - bgs * bg2);
                         const float w = alpha * T;
@@ -413,15 +414,29 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
                     }
                 }
                 if (__any_sync(0xffffffffu, any)) {
+                    // transpose-reduce of fields 0..7 (4 + 2 + 1 + 1 + 1 shuffles): afterwards
+                    // lane L (L & 3 == 0) holds the warp sum of field ((L >> 2) & 7); field 8
+                    // by a plain butterfly (5 shuffles)
+                    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+                    float v4[4], v2[2];
 #pragma unroll
-                    for (int f = 0; f < 9; ++f) {
-#pragma unroll
-                        for (int o = 16; o > 0; o >>= 1) g[f] += __shfl_xor_sync(0xffffffffu, g[f], o);
+                    for (int j = 0; j < 4; ++j) {
+                        const float send = h16 ? g[j] : g[4 + j];
+                        v4[j] = (h16 ? g[4 + j] : g[j]) + __shfl_xor_sync(0xffffffffu, send, 16);
                     }
-                    if (lane == 0) {
 #pragma unroll
-                        for (int f = 0; f < 9; ++f) atomicAdd(&s_acc[f][k], g[f]);
+                    for (int j = 0; j < 2; ++j) {
+                        const float send = h8 ? v4[j] : v4[2 + j];
+                        v2[j] = (h8 ? v4[2 + j] : v4[j]) + __shfl_xor_sync(0xffffffffu, send, 8);
                     }
+                    float v1 = (h4 ? v2[1] : v2[0]) + __shfl_xor_sync(0xffffffffu, h4 ? v2[0] : v2[1], 4);
+                    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+                    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+                    float v8 = g[8];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, o);
+                    if ((lane & 3) == 0) atomicAdd(&s_acc[(lane >> 2) & 7][k], v1);
+                    if (lane == 1) atomicAdd(&s_acc[8][k], v8);
                 }
             }
             if (act) {
