@@ -402,17 +402,18 @@ def run_ours(args):
         b.record(stream)
         torch.cuda.synchronize()
         ms_b = dist.max_over_ranks(a.elapsed_time(b))
+        n_grad = int((grad2d != 0).any(dim=1).sum().item())   # Gaussians blended in the last view
         rb_ms = sum(e[2].elapsed_time(e[3]) for e in bev) / n_bw
         pb_ms = sum(e[3].elapsed_time(e[4]) for e in bev) / n_bw
         Pb = float(np.mean([pairs[v] for v in my_views[:n_bw]]))
         NVb = float(np.mean([nvis[v] for v in my_views[:n_bw]]))
         # algorithmic bytes: render backward reads id + record per pair, dL/dC + T + n_contrib per
         # pixel, and adds 36 B of gradient per (tile, Gaussian) pair; preprocess backward reads the
-        # 48 B grad2d row of every Gaussian, and per visible one its parameters (48 B + SH) and
-        # read-modify-writes its gradients (48 B + SH)
+        # 48 B grad2d row of every Gaussian, and per Gaussian with a non-zero row (blended somewhere
+        # in the view) its parameters (48 B + SH) and a read-modify-write of its gradients (48 B + SH)
         rb_bytes = 40 * Pb + 20 * W * H + 2 * 36 * Pb
-        pb_bytes = 48 * ds.n + NVb * (48 + 4 * sh_floats) + 2 * NVb * (48 + 4 * sh_floats)
-        bw_info = {"views_per_s": world * n_bw / (ms_b / 1e3), "views": world * n_bw,
+        pb_bytes = 48 * ds.n + 3 * n_grad * (48 + 4 * sh_floats)
+        bw_info = {"views_per_s": world * n_bw / (ms_b / 1e3), "views": world * n_bw, "blended_gaussians": n_grad,
                    "note": "per view: a1-a6 with T_final / n_contrib, grad2d zeroing, ss_render_backward, "
                            "ss_preprocess_backward (dL/dC uniform random, resident)",
                    "render_backward": {"ms": rb_ms, "bound": "hbm", "bytes": rb_bytes,

@@ -329,9 +329,10 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
     __shared__ float s_dC[3][256];
     __shared__ float s_Tfin[256];
     __shared__ uint32_t s_id[kBatch];
-    __shared__ float s_acc[9][kBatch + 1];  // +1: the 8 field rows in distinct banks
+    __shared__ uint32_t s_wmask[8][kBatch / 32];  // per warp: batch slots it wrote partials for
     __shared__ uint32_t s_warp[8];
     __shared__ uint32_t s_max;
+    extern __shared__ float s_part[];              // [8 warps][kBatch][9] per-warp partial sums
     const int tile = blockIdx.x;
     int mpx, mpy;
     tile_pixel(tile, tiles_x, threadIdx.x, mpx, mpy);
@@ -347,7 +348,6 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
     s_dC[0][threadIdx.x] = inside ? dimg[pix] : 0.0f;
     s_dC[1][threadIdx.x] = inside ? dimg[plane + pix] : 0.0f;
     s_dC[2][threadIdx.x] = inside ? dimg[2 * plane + pix] : 0.0f;
-    for (int k = threadIdx.x; k < 9 * (kBatch + 1); k += 256) (&s_acc[0][0])[k] = 0.0f;
     __syncthreads();
     if (my_last) atomicMax(&s_max, my_last);
     __syncthreads();
@@ -360,7 +360,8 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
         load_batch(s, vals, rec, start + threadIdx.x, end, s_id);
         __syncthreads();
         const uint32_t n_warps = (n_active + 31) / 32;
-        if ((uint32_t)(threadIdx.x >> 5) < n_warps) {
+        const int warp = threadIdx.x >> 5;
+        if ((uint32_t)warp < n_warps) {
             const bool act = threadIdx.x < n_active;
             const int pp = act ? st.list[threadIdx.x] : 0;
             int px, py;
@@ -368,6 +369,8 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
             const float fpx = (float)px, fpy = (float)py;
             const uint32_t plast = act ? st.last[pp] : 0u;
             const float Tfin = s_Tfin[pp];
+            float *wpart = s_part + (size_t)warp * kBatch * 9;
+            uint32_t wm0 = 0, wm1 = 0, wm2 = 0, wm3 = 0;  // slots this warp wrote (warp-uniform)
             const float dC0 = s_dC[0][pp], dC1 = s_dC[1][pp], dC2 = s_dC[2][pp];
             float T = st.T[pp];
             float S0 = st.C0[pp], S1 = st.C1[pp], S2 = st.C2[pp];
@@ -435,9 +438,20 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
                     float v8 = g[8];
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, o);
-                    if ((lane & 3) == 0) atomicAdd(&s_acc[(lane >> 2) & 7][k], v1);
-                    if (lane == 1) atomicAdd(&s_acc[8][k], v8);
+                    if ((lane & 3) == 0) wpart[k * 9 + ((lane >> 2) & 7)] = v1;
+                    if (lane == 1) wpart[k * 9 + 8] = v8;
+                    const uint32_t bit = 1u << (k & 31);
+                    wm0 |= (k >> 5) == 0 ? bit : 0u;
+                    wm1 |= (k >> 5) == 1 ? bit : 0u;
+                    wm2 |= (k >> 5) == 2 ? bit : 0u;
+                    wm3 |= (k >> 5) == 3 ? bit : 0u;
                 }
+            }
+            if (lane == 0) {
+                s_wmask[warp][0] = wm0;
+                s_wmask[warp][1] = wm1;
+                s_wmask[warp][2] = wm2;
+                s_wmask[warp][3] = wm3;
             }
             if (act) {
                 st.T[pp] = T;
@@ -449,13 +463,21 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
         __syncthreads();
         if ((int)threadIdx.x < cnt) {
             const int k = threadIdx.x;
-            const float4 a0 = make_float4(s_acc[0][k], s_acc[1][k], s_acc[2][k], s_acc[3][k]);
-            const float4 a1 = make_float4(s_acc[4][k], s_acc[5][k], s_acc[6][k], s_acc[7][k]);
-            const float a2 = s_acc[8][k];
+            float a[9];
 #pragma unroll
-            for (int f = 0; f < 9; ++f) s_acc[f][k] = 0.0f;
-            if (a0.x != 0.f || a0.y != 0.f || a0.z != 0.f || a0.w != 0.f || a1.x != 0.f || a1.y != 0.f ||
-                a1.z != 0.f || a1.w != 0.f || a2 != 0.f) {
+            for (int f = 0; f < 9; ++f) a[f] = 0.0f;
+            bool hit = false;
+            for (uint32_t w = 0; w < n_warps; ++w) {
+                if (!((s_wmask[w][k >> 5] >> (k & 31)) & 1u)) continue;
+                const float *src = s_part + ((size_t)w * kBatch + k) * 9;
+#pragma unroll
+                for (int f = 0; f < 9; ++f) a[f] += src[f];
+                hit = true;
+            }
+            const float4 a0 = make_float4(a[0], a[1], a[2], a[3]);
+            const float4 a1 = make_float4(a[4], a[5], a[6], a[7]);
+            const float a2 = a[8];
+            if (hit) {
                 float4 *gp = grad2d + 3 * (size_t)s_id[k];
                 atomicAdd(gp + 0, a0);
                 atomicAdd(gp + 1, a1);
@@ -562,7 +584,11 @@ cudaError_t launch_render_backward(void *ws, const Layout &L, int W, int H, floa
                                    cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
-    launch_pdl(k_render_backward, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges),
+    static int smem_done[64] = {0};
+    const size_t smem = sizeof(float) * 8 * kBatch * 9;
+    cudaError_t e = ensure_smem(k_render_backward, smem, smem_done);
+    if (e != cudaSuccess) return e;
+    launch_pdl(k_render_backward, P.n_tiles, 256, smem, st, at<const uint2>(ws, P.ranges),
                at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
                dimg, T_final, n_contrib, reinterpret_cast<float4 *>(grad2d));
     return cudaGetLastError();
