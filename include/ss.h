@@ -210,7 +210,7 @@ SS_API ss_status ss_compact_scene(const ss_scene *in /*host*/, const uint8_t *ke
 /* ---- NEXT-2: backward of the forward path ("the per-pixel gradients from the render
  * kernel are parallelized and aggregated to the 2D mu_2D and Sigma_2D parameters, which are
  * then parallelized across Gaussians to compute gradients for mu and s").  The gradient is
- * the derivative of the forward above where it is differentiable (reading R25):
+ * the derivative of the forward above where it is differentiable (reading R27):
  * a clamped alpha (0.99), a clamped J entry and a clamped colour pass nothing through the
  * clamped quantity; t, the tile sets and the depth order carry no gradient.
  *

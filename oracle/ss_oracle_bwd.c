@@ -14,7 +14,7 @@
  *   conic (a, b, c) = Sigma_2D^-1 (Eq. 10, R24 order), q = a dx^2 + 2 b dx dy + c dy^2
  *   alpha = min(0.99, sigma exp(-q/2)) (Eq. 5, R16);  c = max(0, sum_k Y_k(dir) h_k + 0.5)
  *   C = sum_i c_i alpha_i T_i + bg T_final,  T_i = prod_{j<i} (1 - alpha_j)            (Eq. 7)
- * Reading R25: the gradient is the derivative of that function where it is
+ * Reading R27: the gradient is the derivative of that function where it is
  * differentiable: a clamped alpha (0.99), a clamped J entry (|p.x/p.z| at the clip) and a
  * clamped colour (c = 0) pass no gradient through the clamped quantity; skipped (alpha <
  * 1/255) and non-blended (terminating, later) Gaussians contribute nothing; t and the tile
@@ -222,7 +222,7 @@ void or_project_f64(int n, int deg, const double *mean_opac, const double *scale
  * stop before blending when T(1-alpha) < 1e-4; C = sum c alpha T + T bg).  Window
  * [x0,x1) x [y0,y1).  blend_hash (optional) receives a hash of the set of blended (pixel,
  * Gaussian) pairs: the finite-difference pins only use steps that leave that set unchanged
- * (the loss jumps where a pixel crosses alpha = 1/255 or the 1e-4 stop, R25). */
+ * (the loss jumps where a pixel crosses alpha = 1/255 or the 1e-4 stop, R27). */
 static const double *g_depth;
 static int cmp_depth(const void *pa, const void *pb)
 {
@@ -398,7 +398,7 @@ void or_render_backward_tiles(const float *rec, const uint32_t *values, const ui
  *   Eq. 4:   Sigma_2D = T Sigma_3D T^T with T = J W:
  *            dL/dSigma_3D = T^T G T,   dL/dT = 2 G T Sigma_3D,  G = [[gxx, gxy/2], [gxy/2, gyy]]
  *   J:       dL/dJ = dL/dT W^T;  J00 = fx/z, J02 = -fx txc/z, J11 = fy/z, J12 = -fy tyc/z,
- *            txc = clamp(x/z) (constant when clamped, R5/R25)
+ *            txc = clamp(x/z) (constant when clamped, R5/R27)
  *   mean:    x2d = fx x/z + cx, y2d = fy y/z + cy;  dL/dmu += W^T dL/dp
  *   Eq. 3:   Sigma_3D = M M^T, M = R S:  dL/dM = 2 dL/dSigma_3D M;  dL/ds_k = sum_r dL/dM_rk R_rk;
  *            dL/dR_rk = dL/dM_rk s_k;  R(qn) written-out partials;  qn = q/|q|:

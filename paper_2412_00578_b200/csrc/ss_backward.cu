@@ -5,7 +5,7 @@
 // s".  This is the second half: one thread per Gaussian takes its accumulated 2D gradient
 // (grad2d, written by ss_render_backward) and applies the chain rule of the forward of
 // ss_preprocess (Eqs. 3-4, 10, the SH colour R13, the J clamp R5; clamped quantities pass
-// nothing, reading R25):
+// nothing, reading R27):
 //   colour   dL/dh_k,ch = dL/dc_ch Y_k (c_ch unclamped); dL/du via dY/du; u = d/|d|
 //   conic    (a, b, c) = (cyy, -cxy, cxx)/det  ->  dL/d(cxx, cxy, cyy)
 //   Eq. 4    Sigma_2D = T Sigma_3D T^T, T = J W: dL/dSigma_3D = T^T G T, dL/dT = 2 G T Sigma_3D

@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
 //   dL/dc_i     = dL/dC alpha_i T_i
 //   unclamped alpha = sigma G:  dL/dsigma = dL/dalpha G,  dL/dq = -dL/dalpha alpha / 2,
 //   dq/dx2d = -2 (a dx + b dy), dq/dy2d = -2 (b dx + c dy), dq/d(a, b, c) = (dx^2, 2 dx dy, dy^2)
-// (a clamped alpha passes nothing to sigma and the geometry, reading R25).  The alpha of
+// (a clamped alpha passes nothing to sigma and the geometry, reading R27).  The alpha of
 // every entry is recomputed with k_render's exact operations, so the blended set is the
 // forward's.  Per batch, each warp reduces a Gaussian's 9 partials by shuffles (only when
 // one of its pixels contributes) into shared-memory accumulators; the CTA then adds each

@@ -1,7 +1,7 @@
 """Pins of the oracle's render backward and preprocess backward (SURVEY §8(f) NEXT-2
 "the per-pixel gradients from the render kernel are ... aggregated to the 2D mu_2D and
 Sigma_2D parameters, which are then parallelized across Gaussians to compute gradients for
-mu and s"; DESIGN.md §3 reading R25).
+mu and s"; DESIGN.md §3 reading R27).
 
 The backward is pinned against things other than itself:
   * central finite differences of the float64 forward (or_loss_f64 / or_project_f64),
@@ -26,7 +26,7 @@ def rec64_of(rec):
 def central_difference(fn, set_x, x0, h0):
     """Central difference of fn (returning (value, blend-set hash)) at x0, with a step that
     leaves the blended (pixel, Gaussian) set unchanged (the loss jumps where a pixel crosses
-    alpha = 1/255, R25); None when no step down to h0/16^3 does."""
+    alpha = 1/255, R27); None when no step down to h0/16^3 does."""
     set_x(x0)
     _, h_mid = fn()
     h = h0
@@ -108,7 +108,7 @@ def test_single_gaussian_closed_form():
 
 
 def test_clamped_alpha_passes_no_gradient():
-    """R25: alpha = min(0.99, sigma G) at the clamp has zero derivative w.r.t. sigma and the
+    """R27: alpha = min(0.99, sigma G) at the clamp has zero derivative w.r.t. sigma and the
     2-D geometry; the colour derivative alpha T remains."""
     rec = np.zeros((1, 12), np.float32)
     rec[0] = [0.0, 0.0, 1.0, 0.05, 0.0, 0.05, 0.999, 2 * np.log(255 * 0.999), 0.7, 0.2, 0.4, 1.0]
