@@ -76,6 +76,8 @@ def lib():
             "or_render_backward": (None, [vp, vp, vp, i, i, vp, vp, i, i, i, i, vp, vp]),
             "or_render_backward_tiles": (None, [vp, vp, vp, i, i, vp, vp, vp, i, vp, vp]),
             "or_project_backward": (None, [i, i, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+            "or_l1_loss_grad": (d, [C.c_int64, vp, vp, vp]),
+            "or_adam_step": (None, [C.c_int64, vp, vp, vp, vp, vp, vp, vp, d, d, d, C.c_int32]),
             "or_frame": (u64, [i, i, vp, vp, vp, vp, vp, i, vp, vp, vp, vp, vp, vp, vp, u64, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
@@ -371,3 +373,27 @@ def project_backward(scene, cam, g2d):
     lib().or_project_backward(n, scene.sh_degree, _p(mo), _p(sc), _p(ro), _p(sh), C.byref(camera(cam)), _p(g2d),
                               _p(dmo), _p(ds), _p(dr), _p(dsh))
     return dmo, ds, dr, dsh
+
+
+# ---- NEXT-3: L1 loss gradient and the Adam step (ss_oracle_bwd.c) -----------------------
+def l1_loss_grad(img, gt):
+    """(L, dL/dimg float32) for L = mean |img - gt|."""
+    img = np.ascontiguousarray(img, np.float32)
+    gt = np.ascontiguousarray(gt, np.float32)
+    g = np.zeros_like(img)
+    L = lib().or_l1_loss_grad(img.size, _p(img), _p(gt), _p(g))
+    return L, g
+
+
+def adam_step(grad_act, raw, m, v, act_of, lr_of, b1=0.9, b2=0.999, eps=1e-15, t=1):
+    """One Adam step on float64 arrays (raw, m, v updated in place); returns the activated
+    parameters.  act_of: 0 identity, 1 exp, 2 sigmoid (per element); lr_of per element."""
+    arrs = [np.ascontiguousarray(a, np.float64) for a in (grad_act, raw, m, v)]
+    for a, src in zip(arrs[1:], (raw, m, v)):
+        assert a is src, "raw / m / v must be C-contiguous float64 (updated in place)"
+    out = np.zeros_like(arrs[1])
+    act = np.ascontiguousarray(np.broadcast_to(act_of, arrs[1].shape), np.int32)
+    lr = np.ascontiguousarray(np.broadcast_to(lr_of, arrs[1].shape), np.float64)
+    lib().or_adam_step(arrs[1].size, _p(arrs[0]), _p(arrs[1]), _p(arrs[2]), _p(arrs[3]), _p(out), _p(act), _p(lr),
+                       b1, b2, eps, t)
+    return out

@@ -522,3 +522,49 @@ void or_project_backward(int n, int deg, const double *mean_opac, const double *
         for (int k = 0; k < 4; ++k) drot[4 * (size_t)i + k] += (dqn[k] - f.qn[k] * qd) / f.qlen;
     }
 }
+
+/* ------------------------------------------------------------------------------------
+ * NEXT-3 (pruning-in-the-loop training on synthetic targets): the two pieces of Eq. 2's
+ * optimisation step that surround the backward.
+ *
+ * L1 loss (Eq. 2's L_1 term; the D-SSIM term is omitted):
+ *   L = (1/K) sum_k |img_k - gt_k|,  dL/dimg_k = sign(img_k - gt_k) / K  (sign(0) = 0),
+ * K = number of values (3 H W).  Returns L (float64); writes dL/dimg as float32.
+ * ---------------------------------------------------------------------------------- */
+double or_l1_loss_grad(int64_t count, const float *img, const float *gt, float *grad)
+{
+    double L = 0.0;
+    for (int64_t k = 0; k < count; ++k) {
+        double d = (double)img[k] - (double)gt[k];
+        L += fabs(d);
+        grad[k] = (float)((d > 0.0 ? 1.0 : (d < 0.0 ? -1.0 : 0.0)) / (double)count);
+    }
+    return count ? L / (double)count : 0.0;
+}
+
+/* Adam (Kingma & Ba; the optimiser of 3D-GS training, "stochastic gradient descent")
+ * on the raw parameters of one array, float64:
+ *   g_raw = g * dact/draw      (act: 0 identity, 1 exp (scales), 2 sigmoid (opacity))
+ *   m = b1 m + (1 - b1) g_raw;  v = b2 v + (1 - b2) g_raw^2
+ *   raw -= lr (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)
+ *   out = act(raw)             (the activated parameter the forward reads, R24)
+ * act and lr are per element (act_of[k], lr_of[k]) so one call covers a whole scene array. */
+void or_adam_step(int64_t count, const double *grad_act, double *raw, double *m, double *v, double *out,
+                  const int32_t *act_of, const double *lr_of, double b1, double b2, double eps, int32_t t)
+{
+    double c1 = 1.0 - pow(b1, t), c2 = 1.0 - pow(b2, t);
+    for (int64_t k = 0; k < count; ++k) {
+        double a;
+        if (act_of[k] == 1) a = exp(raw[k]);
+        else if (act_of[k] == 2) a = 1.0 / (1.0 + exp(-raw[k]));
+        else a = raw[k];
+        double d = act_of[k] == 1 ? a : (act_of[k] == 2 ? a * (1.0 - a) : 1.0);
+        double g = grad_act[k] * d;
+        m[k] = b1 * m[k] + (1.0 - b1) * g;
+        v[k] = b2 * v[k] + (1.0 - b2) * g * g;
+        raw[k] -= lr_of[k] * (m[k] / c1) / (sqrt(v[k] / c2) + eps);
+        if (act_of[k] == 1) out[k] = exp(raw[k]);
+        else if (act_of[k] == 2) out[k] = 1.0 / (1.0 + exp(-raw[k]));
+        else out[k] = raw[k];
+    }
+}
