@@ -21,5 +21,5 @@ launches)
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --ncu --steps 1 --warmup 1 --views-per-step 2 > /dev/null 2>&1; echo ncu_launches=$?
   python profiles/summarize.py launches gpurun_out/${TAG}_launches.csv ;;
 full)
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_(preprocess|emit|render|onesweep|tile_finalize)' -s 40 -c 12 -o gpurun_out/${TAG}_full python bench.py --ncu --steps 1 --warmup 1 --views-per-step 2 > gpurun_out/${TAG}_full.log 2>&1; echo ncu_full=$? ;;
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_(preprocess|emit|render|onesweep|tile_finalize|render_backward|preprocess_backward)' -s 40 -c 12 -o gpurun_out/${TAG}_full python bench.py --ncu --steps 1 --warmup 1 --views-per-step 2 > gpurun_out/${TAG}_full.log 2>&1; echo ncu_full=$? ;;
 esac; done
