@@ -241,6 +241,34 @@ typedef struct {
 SS_API ss_status ss_preprocess_backward(const ss_scene *scene /*host*/, const ss_camera *cam /*host*/,
                                         const float *grad2d, const ss_scene_grad *grad /*host*/, void *stream);
 
+/* ---- NEXT-3: the optimisation step around the backward (Eq. 2, "optimized via
+ * stochastic gradient descent on image reconstruction losses"; L1 term only, the D-SSIM term
+ * is omitted -- SPEC S:421).
+ *
+ * ss_l1_loss_grad: dL_dimg[k] = sign(img[k] - gt[k]) / count (sign(0) = 0), *loss_sum +=
+ * sum_k |img[k] - gt[k]| (device float64, caller-zeroed; L = loss_sum / count).  count >= 0
+ * float32 values; img, gt, dL_dimg device arrays of `count` floats. */
+SS_API ss_status ss_l1_loss_grad(int64_t count, const float *img, const float *gt, float *dL_dimg, double *loss_sum,
+                                 void *stream);
+
+/* Adam (the 3D-GS optimiser) on RAW parameters: raw = (mean xyz, logit sigma | log s | q | h);
+ * every step reads grad (dL/d ACTIVATED parameter, from ss_preprocess_backward), applies the
+ * activation's derivative (exp for scales, sigmoid for the opacity, identity otherwise),
+ * updates raw, m, v (float32) with bias correction for step t = cfg->step >= 1, and writes the
+ * activated parameters into `scene` (the arrays the forward reads).  SH coefficients 0..2 (DC)
+ * use lr_sh_dc, the rest lr_sh_rest.  ss_adam_init sets raw = act^-1(scene), m = v = 0. All
+ * five arrays share the scene's layout and n / sh_degree. */
+typedef struct {
+    float lr_mean, lr_opacity, lr_scale, lr_rot, lr_sh_dc, lr_sh_rest;
+    float beta1, beta2, eps;
+    int32_t step;
+} ss_adam_config;
+SS_API ss_status ss_adam_init(const ss_scene *scene /*host*/, const ss_scene_grad *raw /*host*/,
+                              const ss_scene_grad *m /*host*/, const ss_scene_grad *v /*host*/, void *stream);
+SS_API ss_status ss_adam_step(const ss_scene_grad *grad /*host*/, const ss_scene_grad *raw /*host*/,
+                              const ss_scene_grad *m /*host*/, const ss_scene_grad *v /*host*/,
+                              const ss_scene_grad *scene /*host*/, const ss_adam_config *cfg /*host*/, void *stream);
+
 /* Convenience: ss_preprocess + ss_bin + ss_sort + ss_render in one call. */
 SS_API ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
                           const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib, void *stream);

@@ -15,7 +15,7 @@ MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}
 EXPORTS = ["ss_frame_workspace_size", "ss_frame_layout", "ss_preprocess", "ss_bin", "ss_sort", "ss_sorted_keys",
            "ss_render", "ss_render_stats", "ss_prune_score", "ss_render_frame",
            "ss_prune_workspace_size", "ss_prune_count", "ss_prune_select", "ss_compact_scene",
-           "ss_render_backward", "ss_preprocess_backward", "ss_status_string", "ss_last_cuda_error", "ss_version"]
+           "ss_render_backward", "ss_preprocess_backward", "ss_l1_loss_grad", "ss_adam_init", "ss_adam_step", "ss_status_string", "ss_last_cuda_error", "ss_version"]
 
 
 class SsScene(C.Structure):
@@ -38,6 +38,11 @@ class SsLayout(C.Structure):
     _fields_ = [(k, C.c_size_t) for k in ("rec", "erec", "depth_key", "order", "sorted_value", "tile_count", "ranges", "n_visible", "total_pairs",
                                           "overflow", "scratch", "total_bytes")] + \
                [(k, C.c_int32) for k in ("tiles_x", "tiles_y", "n_tiles", "tile_bits")]
+
+
+class SsAdamConfig(C.Structure):
+    _fields_ = [(k, C.c_float) for k in ("lr_mean", "lr_opacity", "lr_scale", "lr_rot", "lr_sh_dc", "lr_sh_rest",
+                                         "beta1", "beta2", "eps")] + [("step", C.c_int32)]
 
 
 class SsError(RuntimeError):
@@ -72,6 +77,9 @@ def lib() -> C.CDLL:
             "ss_compact_scene": (st, [P(SsScene), vp, P(SsScene), vp, vp, C.c_size_t, vp]),
             "ss_render_backward": (st, [P(SsFrame), P(C.c_float), vp, vp, vp, vp, vp]),
             "ss_preprocess_backward": (st, [P(SsScene), P(SsCamera), vp, P(SsScene), vp]),
+            "ss_l1_loss_grad": (st, [C.c_int64, vp, vp, vp, vp, vp]),
+            "ss_adam_init": (st, [P(SsScene), P(SsScene), P(SsScene), P(SsScene), vp]),
+            "ss_adam_step": (st, [P(SsScene), P(SsScene), P(SsScene), P(SsScene), P(SsScene), P(SsAdamConfig), vp]),
             "ss_status_string": (C.c_char_p, [st]),
             "ss_last_cuda_error": (C.c_char_p, []),
             "ss_version": (C.c_char_p, []),

@@ -28,6 +28,7 @@ UNITS = {
     "ss_render.cu": [],
     "ss_prune.cu": [],
     "ss_backward.cu": [],
+    "ss_train.cu": [],
 }
 HEADERS = ["ss_common.cuh", "ss_tilegeom.cuh"]
 

@@ -238,6 +238,39 @@ ss_status ss_preprocess_backward(const ss_scene *scene, const ss_camera *cam, co
                                                   static_cast<cudaStream_t>(stream)));
 }
 
+static bool grad_ok(const ss_scene_grad *g, int32_t n, int32_t deg) {
+    if (!g || g->n != n || g->sh_degree != deg) return false;
+    return n == 0 || (g->mean_opac && g->scale && g->rot && g->sh);
+}
+
+ss_status ss_l1_loss_grad(int64_t count, const float *img, const float *gt, float *dL_dimg, double *loss_sum,
+                          void *stream) {
+    if (count < 0 || (count > 0 && (!img || !gt || !dL_dimg || !loss_sum))) return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_l1_loss_grad(count, img, gt, dL_dimg, loss_sum, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_adam_init(const ss_scene *scene, const ss_scene_grad *raw, const ss_scene_grad *m,
+                       const ss_scene_grad *v, void *stream) {
+    if (!scene || scene->n < 0 || scene->sh_degree < 0 || scene->sh_degree > 3) return SS_ERR_INVALID_ARG;
+    if (scene->n > 0 && (!scene->mean_opac || !scene->scale || !scene->rot || !scene->sh)) return SS_ERR_INVALID_ARG;
+    if (!grad_ok(raw, scene->n, scene->sh_degree) || !grad_ok(m, scene->n, scene->sh_degree) ||
+        !grad_ok(v, scene->n, scene->sh_degree))
+        return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_adam_init(*scene, *raw, *m, *v, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_adam_step(const ss_scene_grad *grad, const ss_scene_grad *raw, const ss_scene_grad *m,
+                       const ss_scene_grad *v, const ss_scene_grad *scene, const ss_adam_config *cfg, void *stream) {
+    if (!grad || !cfg || grad->n < 0 || grad->sh_degree < 0 || grad->sh_degree > 3) return SS_ERR_INVALID_ARG;
+    const int32_t n = grad->n, d = grad->sh_degree;
+    if (!grad_ok(grad, n, d) || !grad_ok(raw, n, d) || !grad_ok(m, n, d) || !grad_ok(v, n, d) || !grad_ok(scene, n, d))
+        return SS_ERR_INVALID_ARG;
+    if (cfg->step < 1 || !(cfg->beta1 >= 0.0f && cfg->beta1 < 1.0f) || !(cfg->beta2 >= 0.0f && cfg->beta2 < 1.0f) ||
+        !(cfg->eps >= 0.0f))
+        return SS_ERR_INVALID_ARG;
+    return cuda_status(launch_adam_step(*grad, *raw, *m, *v, *scene, *cfg, static_cast<cudaStream_t>(stream)));
+}
+
 ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
                           const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib, void *stream) {
     ss_status s = ss_preprocess(scene, cam, mode, frame, stream);

@@ -1,5 +1,7 @@
 // ss_common.cuh -- shared device/host definitions of libss (CUDA path only).
 #pragma once
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <utility>
 #include <cuda_runtime.h>
@@ -149,6 +151,13 @@ cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg
 cudaError_t launch_render_backward(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2,
                                    const float *dimg, const float *T_final, const uint32_t *n_contrib, float *grad2d,
                                    cudaStream_t st);
+cudaError_t launch_l1_loss_grad(int64_t count, const float *img, const float *gt, float *grad, double *loss_sum,
+                                cudaStream_t st);
+cudaError_t launch_adam_init(const ss_scene &sc, const ss_scene_grad &raw, const ss_scene_grad &m,
+                             const ss_scene_grad &v, cudaStream_t st);
+cudaError_t launch_adam_step(const ss_scene_grad &g, const ss_scene_grad &raw, const ss_scene_grad &m,
+                             const ss_scene_grad &v, const ss_scene_grad &out, const ss_adam_config &c,
+                             cudaStream_t st);
 cudaError_t launch_preprocess_backward(const ss_scene &sc, const CamArgs &cam, const float *grad2d,
                                        const ss_scene_grad &out, cudaStream_t st);
 

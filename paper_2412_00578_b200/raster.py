@@ -279,27 +279,41 @@ def render_views_to_host(rz: Rasterizer, cams, host_out: list, bg=(0.0, 0.0, 0.0
     st["copy"].synchronize()
 
 
-def prune(scene: DeviceScene, score: torch.Tensor, ratio: float, stream=None) -> tuple[DeviceScene, torch.Tensor]:
-    """The prune step (Sec. 4.2): drop floor(ratio * N) Gaussians with the smallest score (ties:
-    higher index first) and return the compacted scene plus the keep mask.  Every rank that
-    holds the same all-reduced score gets the same scene (no further exchange)."""
-    assert score.dtype == torch.float64 and score.numel() == scene.n and score.is_cuda
-    n = scene.n
+def prune_select(score: torch.Tensor, ratio: float, stream=None) -> tuple[torch.Tensor, int]:
+    """keep mask (uint8, device) removing k = floor(ratio N) Gaussians with the smallest score
+    (ties: higher index first), and k."""
+    assert score.dtype == torch.float64 and score.is_cuda and score.dim() == 1
+    n = score.numel()
     k = int(lib().ss_prune_count(n, float(ratio)))
-    dev = scene.mean_opac.device
-    ws = torch.empty(int(lib().ss_prune_workspace_size(n)), dtype=torch.uint8, device=dev)
-    keep = torch.empty(n, dtype=torch.uint8, device=dev)
-    sh_handle = C.c_void_p(_stream_handle(stream))
+    ws = torch.empty(int(lib().ss_prune_workspace_size(n)), dtype=torch.uint8, device=score.device)
+    keep = torch.empty(n, dtype=torch.uint8, device=score.device)
     check(lib().ss_prune_select(C.c_void_p(score.data_ptr()), n, float(ratio), C.c_void_p(keep.data_ptr()),
-                                C.c_void_p(ws.data_ptr()), ws.numel(), sh_handle), "ss_prune_select")
-    m = n - k
+                                C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(_stream_handle(stream))),
+          "ss_prune_select")
+    return keep, k
+
+
+def compact(scene: DeviceScene, keep: torch.Tensor, n_keep: int, stream=None) -> DeviceScene:
+    """Stable stream compaction of every array of a scene-shaped set (scene, or optimiser
+    state with the scene's layout) by `keep` (ss_compact_scene)."""
+    n, m, dev = scene.n, int(n_keep), scene.mean_opac.device
     out = DeviceScene(torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
                       torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
                       torch.empty((max(m, 1), 4), dtype=torch.float32, device=dev)[:m],
                       torch.empty((m, scene.sh.shape[1], 4), dtype=torch.float32, device=dev), scene.sh_degree)
+    ws = torch.empty(int(lib().ss_prune_workspace_size(n)), dtype=torch.uint8, device=dev)
     n_out = torch.zeros(1, dtype=torch.int32, device=dev)
     src, dst = scene.struct(), out.struct()
     check(lib().ss_compact_scene(C.byref(src), C.c_void_p(keep.data_ptr()), C.byref(dst),
-                                 C.c_void_p(n_out.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(), sh_handle),
-          "ss_compact_scene")
-    return out, keep
+                                 C.c_void_p(n_out.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(),
+                                 C.c_void_p(_stream_handle(stream))), "ss_compact_scene")
+    return out
+
+
+def prune(scene: DeviceScene, score: torch.Tensor, ratio: float, stream=None) -> tuple[DeviceScene, torch.Tensor]:
+    """The prune step (Sec. 4.2): drop floor(ratio * N) Gaussians with the smallest score (ties:
+    higher index first) and return the compacted scene plus the keep mask.  Every rank that
+    holds the same all-reduced score gets the same scene (no further exchange)."""
+    assert score.numel() == scene.n
+    keep, k = prune_select(score, ratio, stream)
+    return compact(scene, keep, scene.n - k, stream), keep

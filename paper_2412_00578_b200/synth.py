@@ -326,3 +326,21 @@ def grad_scene(n=40, width=72, height=40, seed=7, opac=(0.05, 0.5), px_sigma=(1.
     q = rng.standard_normal((n, 4))
     q *= rng.uniform(0.5, 2.0, (n, 1)) / np.linalg.norm(q, axis=1, keepdims=True)  # non-unit: normalised in-kernel
     return Scene(mean_opac, sc, q.astype(np.float32), _sh_planes(rng, n, sh_degree), sh_degree, "grad"), cam
+
+
+def perturb(scene: Scene, seed=1, mean_sd=0.01, logit_sd=0.5, dc_sd=0.2, log_scale_sd=0.2) -> Scene:
+    """A noisy copy of `scene` (NEXT-3 training init): means + N(0, mean_sd), opacity logits
+    + N(0, logit_sd), SH DC + N(0, dc_sd), log-scales + N(0, log_scale_sd)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n = scene.n
+    mo = scene.mean_opac.astype(np.float64).copy()
+    mo[:, :3] += rng.normal(0, mean_sd, (n, 3))
+    o = np.clip(mo[:, 3], 1e-4, 1 - 1e-4)
+    logit = np.log(o / (1 - o)) + rng.normal(0, logit_sd, n)
+    mo[:, 3] = 1.0 / (1.0 + np.exp(-logit))
+    sc = scene.scale.astype(np.float64).copy()
+    sc[:, :3] *= np.exp(rng.normal(0, log_scale_sd, (n, 3)))
+    sh = scene.sh.copy()
+    sh[0, :, :3] += rng.normal(0, dc_sd, (n, 3)).astype(np.float32)
+    return Scene(mo.astype(np.float32), sc.astype(np.float32), scene.rot.copy(), sh, scene.sh_degree,
+                 scene.name + "-perturbed")

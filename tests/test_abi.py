@@ -20,7 +20,7 @@ def lib():
 
 def test_exports_match_header(lib):
     hdr = open(os.path.join(ROOT, "include", "ss.h")).read()
-    declared = set(re.findall(r"^\s*(?:SS_API\s+)?(?:const\s+)?[a-z_0-9]+\s*\*?\s*(ss_[a-z_]+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:SS_API\s+)?(?:const\s+)?[a-z_0-9]+\s*\*?\s*(ss_[a-z_0-9]+)\s*\(", hdr, re.M))
     assert declared == set(_abi.EXPORTS), declared ^ set(_abi.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
