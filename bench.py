@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-score", action="store_true")
     ap.add_argument("--no-backward", action="store_true")
+    ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="short run for profilers: no clocks/e2e/cpu legs")
     return ap.parse_args()
 
@@ -424,6 +425,43 @@ def run_ours(args):
                                            "unit": "GB/s", "frac": pb_bytes / (pb_ms / 1e3) / 1e9 / hbm_peak}}
         del grad2d, grads
 
+    # ---- training step (NEXT-3): a1-a6 + L1 + render backward + preprocess backward + Adam
+    train_info = None
+    if not args.no_train and not args.ncu and prune_info is None:
+        from paper_2412_00578_b200.train import AdamConfig, Trainer
+        n_tv = min(len(my_views), 8)
+        tcams = [cams[v] for v in my_views[:n_tv]]
+        targets = [torch.zeros((3, H, W), dtype=torch.float32, device=dev).uniform_(0, 1) for _ in tcams]
+        tscene = DeviceScene(ds.mean_opac.clone(), ds.scale.clone(), ds.rot.clone(), ds.sh.clone(), ds.sh_degree)
+        tr = Trainer(tscene, tcams, targets, adam=AdamConfig(extent=4.0), check_overflow=False)
+        for j in range(3):
+            tr.step(j % n_tv)
+        n_it = max(8, args.steps)
+        aev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_it)]
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for j in range(n_it):
+            tr.events = aev[j]
+            tr.step(j % n_tv)
+        b.record(stream)
+        torch.cuda.synchronize()
+        tr.events = None
+        ms_t = dist.max_over_ranks(a.elapsed_time(b))
+        adam_ms = sum(x.elapsed_time(y) for x, y in aev) / n_it
+        # Adam: per Gaussian reads grad, raw, m, v and writes raw, m, v, the activated array:
+        # 8 passes over the scene's 240 B (mean_opac, scale, rot, 12 SH float4)
+        adam_bytes = 8 * 16 * (3 + {0: 1, 1: 3, 2: 7, 3: 12}[scene.sh_degree]) * ds.n
+        train_info = {"iters_per_s": world * n_it / (ms_t / 1e3), "iters": world * n_it,
+                      "note": "one view per iteration (replica per rank): a1-a6 with T/n_contrib, ss_l1_loss_grad, "
+                              "ss_render_backward, ss_preprocess_backward, ss_adam_step over all N Gaussians "
+                              "(dense Adam, as 3D-GS); targets uniform random; capacity sized up front",
+                      "adam": {"ms": adam_ms, "bound": "hbm", "bytes": adam_bytes,
+                               "achieved": adam_bytes / (adam_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                               "frac": adam_bytes / (adam_ms / 1e3) / 1e9 / hbm_peak}}
+        del tr, tscene, targets
+
     # ---- end to end through the public API: camera in, image out to pinned host memory
     e2e = None
     if not args.no_e2e and not args.ncu:
@@ -481,6 +519,7 @@ def run_ours(args):
             "e2e": e2e,
             "prune_score": score_info,
             "backward": bw_info,
+            "train": train_info,
             "cpu_baseline": cpu,
             "paper_context": {"gpu": "RTX A5000 (PAPER.md P:447)", "accutile_fps_avg_scene": 267,
                               "speedups": {"snugbox": 1.82, "accutile": 1.99, "overall": 6.71}},

@@ -64,55 +64,51 @@ __device__ __forceinline__ void adam1(float g_act, float &raw, float &m, float &
     out = act_fwd(act, raw);
 }
 
-__device__ __forceinline__ void adam4(const float4 *__restrict__ g, float4 *__restrict__ raw, float4 *__restrict__ m,
-                                      float4 *__restrict__ v, float4 *__restrict__ out, size_t k, const int act[4],
-                                      const float lr[4], int n_used, const AdamArgs &A) {
-    const float4 g4 = g[k];
-    float4 r4 = raw[k], m4 = m[k], v4 = v[k], o4 = out[k];
-    float *gr = (float *)&g4, *rr = (float *)&r4, *mr = (float *)&m4, *vr = (float *)&v4, *orr = (float *)&o4;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-        if (c < n_used) adam1(gr[c], rr[c], mr[c], vr[c], orr[c], act[c], lr[c], A);
-    raw[k] = r4;
-    m[k] = m4;
-    v[k] = v4;
-    out[k] = o4;
-}
-
-// One thread per Gaussian: mean_opac (xyz identity, sigma sigmoid), scale (exp, w unused),
-// rot (identity), SH blocks (identity; DC coefficients 0..2 at lr_sh_dc, the rest at
-// lr_sh_rest; padding components untouched).
-__global__ void __launch_bounds__(256) k_adam(int n, int nb3, int B, ss_scene_grad g, ss_scene_grad raw, ss_scene_grad m,
-                                              ss_scene_grad v, ss_scene_grad out, AdamArgs A) {
+// One thread per float4 of the scene arrays, flat over [mean_opac | scale | rot | sh] (n, n,
+// n, n*B float4), so every array is read and written fully coalesced: grad, raw, m, v are
+// read, raw, m, v and the activated array written (components a slot does not use -- scale.w,
+// SH padding -- keep raw == activated, as ss_adam_init set them).  mean_opac: xyz identity,
+// sigma sigmoid; scale: exp; rot: identity; SH: identity, coefficients 0..2 (DC) at lr_sh_dc.
+__global__ void __launch_bounds__(256) k_adam(int64_t n, int B, int nb3, ss_scene_grad g, ss_scene_grad raw,
+                                              ss_scene_grad m, ss_scene_grad v, ss_scene_grad out, AdamArgs A) {
     pdl_enter();
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
-    {
-        const int act[4] = {0, 0, 0, 2};
-        const float lr[4] = {A.lr_mean, A.lr_mean, A.lr_mean, A.lr_opacity};
-        adam4((const float4 *)g.mean_opac, (float4 *)raw.mean_opac, (float4 *)m.mean_opac, (float4 *)v.mean_opac,
-              (float4 *)out.mean_opac, i, act, lr, 4, A);
-    }
-    {
-        const int act[4] = {1, 1, 1, 1};
-        const float lr[4] = {A.lr_scale, A.lr_scale, A.lr_scale, A.lr_scale};
-        adam4((const float4 *)g.scale, (float4 *)raw.scale, (float4 *)m.scale, (float4 *)v.scale,
-              (float4 *)out.scale, i, act, lr, 3, A);
-    }
-    {
-        const int act[4] = {0, 0, 0, 0};
-        const float lr[4] = {A.lr_rot, A.lr_rot, A.lr_rot, A.lr_rot};
-        adam4((const float4 *)g.rot, (float4 *)raw.rot, (float4 *)m.rot, (float4 *)v.rot, (float4 *)out.rot, i, act,
-              lr, 4, A);
-    }
-    const int act[4] = {0, 0, 0, 0};
-    for (int p = 0; p < B; ++p) {
-        float lr[4];
+    const int64_t total = n * (3 + B);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int arr;
+        int64_t e;
+        if (k < n) { arr = 0; e = k; }
+        else if (k < 2 * n) { arr = 1; e = k - n; }
+        else if (k < 3 * n) { arr = 2; e = k - 2 * n; }
+        else { arr = 3; e = k - 3 * n; }
+        auto pick = [arr](const ss_scene_grad &a) {
+            return reinterpret_cast<float4 *>(arr == 0 ? a.mean_opac : arr == 1 ? a.scale : arr == 2 ? a.rot : a.sh);
+        };
+        float4 *const gp = pick(g), *const rp = pick(raw), *const mp = pick(m), *const vp = pick(v),
+                     *const op = pick(out);
+        const float4 g4 = gp[e];
+        float4 r4 = rp[e];
+        float4 m4 = mp[e];
+        float4 v4 = vp[e];
+        float4 o4;
+        const float *gr = (const float *)&g4;
+        float *rr = (float *)&r4, *mr = (float *)&m4, *vr = (float *)&v4, *orr = (float *)&o4;
+        const int coef0 = arr == 3 ? (int)(e % B) * 4 : 0;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) lr[c] = (4 * p + c) < 3 ? A.lr_sh_dc : A.lr_sh_rest;
-        const int used = min(4, nb3 - 4 * p);
-        adam4((const float4 *)g.sh, (float4 *)raw.sh, (float4 *)m.sh, (float4 *)v.sh, (float4 *)out.sh,
-              (size_t)i * B + p, act, lr, used, A);
+        for (int c = 0; c < 4; ++c) {
+            int act = 0, used = 1;
+            float lr;
+            if (arr == 0) { act = c == 3 ? 2 : 0; lr = c == 3 ? A.lr_opacity : A.lr_mean; }
+            else if (arr == 1) { act = 1; used = c < 3; lr = A.lr_scale; }
+            else if (arr == 2) { lr = A.lr_rot; }
+            else { used = coef0 + c < nb3; lr = coef0 + c < 3 ? A.lr_sh_dc : A.lr_sh_rest; }
+            if (used) adam1(gr[c], rr[c], mr[c], vr[c], orr[c], act, lr, A);
+            else orr[c] = rr[c];
+        }
+        rp[e] = r4;
+        mp[e] = m4;
+        vp[e] = v4;
+        op[e] = o4;
     }
 }
 
@@ -177,7 +173,10 @@ cudaError_t launch_adam_step(const ss_scene_grad &g, const ss_scene_grad &raw, c
     A.c1 = (float)(1.0 - std::pow((double)c.beta1, (double)c.step));
     A.c2 = (float)(1.0 - std::pow((double)c.beta2, (double)c.step));
     const int nb3 = (g.sh_degree + 1) * (g.sh_degree + 1) * 3;
-    launch_pdl(k_adam, (g.n + 255) / 256, 256, 0, st, g.n, nb3, sh_blocks(g.sh_degree), g, raw, m, v, out, A);
+    const int B = sh_blocks(g.sh_degree);
+    const int64_t total = (int64_t)g.n * (3 + B);
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
+    launch_pdl(k_adam, blocks, 256, 0, st, (int64_t)g.n, B, nb3, g, raw, m, v, out, A);
     return cudaGetLastError();
 }
 

@@ -69,7 +69,9 @@ class Trainer:
     """Scene + Adam state on the device; one Rasterizer workspace reused across views."""
 
     def __init__(self, scene: DeviceScene, cams, targets: list[torch.Tensor], bg=(0.0, 0.0, 0.0),
-                 mode: str = "accutile", adam: AdamConfig | None = None, seed: int = 0):
+                 mode: str = "accutile", adam: AdamConfig | None = None, seed: int = 0,
+                 check_overflow: bool = True):
+        self.check_overflow = check_overflow   # False: capacity sized up front, no per-step read-back
         self.cams = list(cams)
         self.targets = targets
         self.bg = tuple(float(b) for b in bg)
@@ -78,6 +80,7 @@ class Trainer:
         self.W, self.H = int(self.cams[0].width), int(self.cams[0].height)
         self.cstructs = [camera_struct(c) for c in self.cams]
         self.it = 0
+        self.events = None     # optional (start, end) CUDA events around the Adam step (bench)
         self.gen = torch.Generator().manual_seed(seed)
         self._set_scene(scene, init_state=True)
         self.loss_sum = torch.zeros(1, dtype=torch.float64, device=self.dev)
@@ -89,8 +92,8 @@ class Trainer:
         self.dev = scene.mean_opac.device
         cap = max(1024, 8 * scene.n)
         self.rz = Rasterizer(scene, self.W, self.H, mode=self.mode, capacity=cap)
-        for c in self.cams[: min(4, len(self.cams))]:
-            self.rz.ensure_capacity(c)
+        for c in (self.cams if not getattr(self, "check_overflow", True) else self.cams[: min(4, len(self.cams))]):
+            self.rz.ensure_capacity(c, headroom=1.5)
         self.grads = scene.zeros_like()
         self.grad2d = torch.zeros((scene.n, 12), dtype=torch.float32, device=self.dev)
         if init_state:
@@ -113,7 +116,8 @@ class Trainer:
             view = int(torch.randint(len(self.cams), (1,), generator=self.gen))
         self.it += 1
         cam = self.cstructs[view]
-        img, T, nc = self.rz.render_frame(cam, self.bg, want_T=True, want_ncontrib=True)
+        img, T, nc = self.rz.render_frame(cam, self.bg, want_T=True, want_ncontrib=True,
+                                          check_overflow=self.check_overflow)
         check(lib().ss_l1_loss_grad(img.numel(), C.c_void_p(img.data_ptr()), C.c_void_p(self.targets[view].data_ptr()),
                                     C.c_void_p(self.dimg.data_ptr()), C.c_void_p(self.loss_sum.data_ptr()),
                                     C.c_void_p(_stream_handle(None))), "ss_l1_loss_grad")
@@ -122,12 +126,16 @@ class Trainer:
         for t in (self.grads.mean_opac, self.grads.scale, self.grads.rot, self.grads.sh):
             t.zero_()
         self.rz.preprocess_backward(cam, self.grad2d, self.grads)
+        if self.events is not None:
+            self.events[0].record()
         cfg = self.adam.struct(self.it)
         sc = self.scene
         out = DeviceScene(sc.mean_opac, sc.scale, sc.rot, sc.sh, sc.sh_degree)
         check(lib().ss_adam_step(C.byref(self.grads.struct()), C.byref(self.raw.struct()), C.byref(self.m.struct()),
                                  C.byref(self.v.struct()), C.byref(out.struct()), C.byref(cfg),
                                  C.c_void_p(_stream_handle(None))), "ss_adam_step")
+        if self.events is not None:
+            self.events[1].record()
         self.n_loss_values = img.numel()
 
     def take_loss(self) -> float:
