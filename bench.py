@@ -41,6 +41,7 @@ def parse():
     ap.add_argument("--workload", default="mnr360-3m")
     ap.add_argument("--mode", default="accutile", choices=["3sigma", "snugbox", "accutile"])
     ap.add_argument("--views-per-step", type=int, default=64)
+    ap.add_argument("--streams", type=int, default=3, help="concurrent frame workspaces (FramePipeline)")
     ap.add_argument("--prune-ratio", type=float, default=0.0,
                     help="pruned-model regime: score all views (a7 + all_reduce), prune this fraction, bench the rest")
     ap.add_argument("--no-e2e", action="store_true")
@@ -184,7 +185,8 @@ def run_ours(args):
 
     from paper_2412_00578_b200 import dist, synth
     from paper_2412_00578_b200._abi import SsCamera
-    from paper_2412_00578_b200.raster import DeviceScene, Rasterizer, camera_struct, prune, render_views_to_host
+    from paper_2412_00578_b200.raster import (DeviceScene, FramePipeline, Rasterizer, camera_struct, prune,
+                                              render_views_to_host)
 
     rank, world, local = dist.init()
     torch.cuda.set_device(local)
@@ -256,8 +258,9 @@ def run_ours(args):
         if e is not None and all_stages:
             e[4].record(stream)
 
-    for j in range(args.warmup * V):
-        frame(seq[j])
+    pipe = FramePipeline(ds, W, H, mode=args.mode, n_streams=args.streams, capacity=rz.capacity)
+    for j in range(args.warmup):
+        pipe.render_views([cstructs[v] for v in seq[j * V:(j + 1) * V]])
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     if not args.ncu:
@@ -265,8 +268,10 @@ def run_ours(args):
         time.sleep(0.3)
     dist.barrier()
     torch.cuda.synchronize()
-    # K steps, each timed by its own events; the L2 is flushed (256 MB written) between steps,
-    # outside the timed regions, so no step starts with the previous step's data cached
+    # K steps of V views each, timed by events on the caller's stream (the pipeline forks its
+    # streams from it and joins them back); every frame's ss_preprocess is bracketed by events
+    # on its own stream.  The L2 is flushed (256 MB written) between steps, outside the timed
+    # regions, so no step starts with the previous step's data cached.
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     t_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in range(args.steps)]
@@ -275,8 +280,7 @@ def run_ours(args):
     for k in range(args.steps):
         flush.zero_()
         t_ev[k][0].record(stream)
-        for j in range(k * V, (k + 1) * V):
-            frame(timed_views[j], ev[j])
+        pipe.render_views([cstructs[v] for v in timed_views[k * V:(k + 1) * V]], pre_events=ev[k * V:(k + 1) * V])
         t_ev[k][1].record(stream)
     host_ms = (time.perf_counter() - h0) * 1e3 / n_timed
     torch.cuda.synchronize()
@@ -285,7 +289,9 @@ def run_ours(args):
     ms_total = sum(a.elapsed_time(b) for a, b in t_ev)
     ms_max = dist.max_over_ranks(ms_total)
     value = world * n_timed / (ms_max / 1e3)
-    # k_preprocess over the timed region; bin / sort / render from a separate pass of V frames
+    # k_preprocess launch durations over the timed region (concurrent with the other streams'
+    # frames); the per-stage split and the isolated k_preprocess duration come from a separate
+    # single-stream pass of V frames
     pre_ms = sum(ev[j][0].elapsed_time(ev[j][1]) for j in range(n_timed)) / n_timed
     ev2 = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(V)]
     flush.zero_()
@@ -294,7 +300,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     stage_ms = {s: sum(ev2[j][i].elapsed_time(ev2[j][i + 1]) for j in range(V)) / V
                 for i, s in enumerate(stages)}
-    stage_ms["preprocess"] = pre_ms
+    pre_iso_ms = stage_ms["preprocess"]
 
     # ---- per-stage roofline numbers (averages over the timed frames)
     mean = lambda d: float(np.mean([d[v] for v in timed_views]))
@@ -334,8 +340,21 @@ def run_ours(args):
         for k, v in tj.get("kernels", {}).items():
             if k.startswith("k_preprocess"):
                 traffic, traffic_src = v["dram_bytes"], tj.get("source")
-    roof = {"bound": di["bound"], "achieved": di["achieved"], "peak": di["peak"], "unit": di["unit"],
-            "frac": di["frac"], "traffic": traffic, "traffic_source": traffic_src,
+    iso_ach = di["bytes"] / (pre_iso_ms / 1e3) / 1e9
+    # Primary figure: k_preprocess launches timed by events on their stream in the single-stream
+    # pass of the same run (V frames, same views), where a launch has the GPU to itself, so
+    # achieved = algorithmic bytes / launch duration is the kernel's own bandwidth and its share
+    # of the frame matches the ncu launch list.  In the timed region 3 frames are in flight and a
+    # launch shares the SMs and HBM with the other streams' kernels, which stretches its duration
+    # (reported under "in_flight"; the throughput gain is the point of the pipeline).
+    roof = {"bound": di["bound"], "achieved": iso_ach, "peak": di["peak"], "unit": di["unit"],
+            "frac": iso_ach / di["peak"], "traffic": traffic, "traffic_source": traffic_src,
+            "launch_ms": pre_iso_ms, "timing": "CUDA events on the launching stream, single-stream pass of V frames "
+                                               "of the same workload in the same run (L2 flushed before it)",
+            "in_flight": {"launch_ms": pre_ms, "achieved": di["bytes"] / (pre_ms / 1e3) / 1e9,
+                          "frac": di["bytes"] / (pre_ms / 1e3) / 1e9 / di["peak"],
+                          "timing": f"timed region, {args.streams} frames in flight on {args.streams} streams: "
+                                    f"launch durations include sharing the GPU with the other frames"},
             "algorithmic_bytes": di["bytes"], "kernel": "k_preprocess",
             "peak_source": hbm_src if di["bound"] == "hbm" else
             f"derived: 148 SM x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {sm_max:.0f} MHz"}
@@ -468,18 +487,19 @@ def run_ours(args):
         n_e = min(len(my_views), V)
         host = [torch.empty((3, H, W), dtype=torch.float32).pin_memory() for _ in range(n_e)]
         vs = [cams[v] for v in my_views[:n_e]]
-        render_views_to_host(rz, vs, host)
+        render_views_to_host(pipe, vs, host)
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         reps = max(1, args.steps // 4)
         for _ in range(reps):
-            render_views_to_host(rz, vs, host)
+            render_views_to_host(pipe, vs, host)
         dt = dist.max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": world * reps * n_e / dt, "unit": "frames/s",
                "h2d_bytes_per_step": V * ctypes.sizeof(SsCamera), "d2h_bytes_per_step": V * 3 * H * W * 4,
                "note": "scene resident in HBM; per frame the camera goes host->device as kernel arguments and "
-                       "the float32 image device->host into pinned memory (copy overlapped on a side stream)"}
+                       "the float32 image device->host into pinned memory, copied on the frame's own stream "
+                       f"({args.streams} frames in flight: copies overlap the other streams' kernels)"}
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
@@ -501,6 +521,7 @@ def run_ours(args):
                        "n_gaussians": ds.n, "pruned": prune_info, "width": W, "height": H,
                        "views": len(cams), "views_per_step_per_rank": V, "mode": args.mode,
                        "sh_degree": scene.sh_degree, "parallelism": f"view-parallel x{world}",
+                       "frames_in_flight": args.streams,
                        "l2": "flushed between steps (256 MB written outside the timed regions); scene %.0f MB, "
                              "per-frame records %.0f MB" % (ds.n * 240 / 1e6, NVm * 48 / 1e6)},
             "pairs_per_frame": {"mean": Pm, "min": min(pairs.values()), "max": max(pairs.values())},
@@ -511,6 +532,7 @@ def run_ours(args):
             "stages": stage_info,
             "render_work": {"E_pix": mean(E_pix), "E_blend": mean(E_blend), "E_cta": mean(E_cta),
                             "E_kept_after_warp_cull": mean(E_kept), "pixels": W * H},
+            "stages_timing": "single-stream pass of V frames after the timed region (every stage bracketed by events)",
             "roofline": roof,
             # ours per frame: k_preprocess, 4 x k_onesweep, k_escan_reduce, k_escan_apply, k_entries,
             # k_big_entries, k_l1_count, k_l1_scan, k_l1_emit, k_l2_count, k_l2_scan, k_l2_write, k_render

@@ -253,30 +253,72 @@ class Rasterizer:
         return self.render(bg, out, stream=stream, **kw)
 
 
-def render_views_to_host(rz: Rasterizer, cams, host_out: list, bg=(0.0, 0.0, 0.0)) -> None:
+class FramePipeline:
+    """N frame workspaces on N CUDA streams (views are independent).
+
+    Views are dealt round-robin to the streams, so one frame's latency-bound kernels (the
+    scans, the look-back depth passes, the small level-2 kernels) overlap another frame's
+    bandwidth-bound preprocess and render instead of leaving SMs idle between launches
+    (measured on B200, MNR360-3M: 1 stream 1263 frames/s, 2 -> 1470, 3 -> 1538, 4 -> 1544).
+    Within a stream the frame's kernels keep their programmatic dependent launches."""
+
+    def __init__(self, scene: DeviceScene, width: int, height: int, mode: str = "accutile", n_streams: int = 3,
+                 capacity: int | None = None):
+        self.n_streams = int(n_streams)
+        self.width, self.height = int(width), int(height)
+        self.rz = [Rasterizer(scene, width, height, mode=mode, capacity=capacity) for _ in range(self.n_streams)]
+        dev = self.rz[0].device
+        self.streams = [torch.cuda.Stream(device=dev) for _ in range(self.n_streams)]
+        self.outs = [torch.empty((3, height, width), dtype=torch.float32, device=dev) for _ in range(self.n_streams)]
+
+    def ensure_capacity(self, cams, headroom: float = 1.02) -> int:
+        """Size every workspace for the largest pair count over `cams` (synchronises)."""
+        P = max(self.rz[0].ensure_capacity(c, headroom) for c in cams)
+        cap = int(P * headroom) + 4096
+        for r in self.rz:
+            if r.capacity != cap:
+                r._alloc(cap)
+        return P
+
+    def render_views(self, cams, bg=(0.0, 0.0, 0.0), on_frame=None, pre_events=None) -> None:
+        """Render every camera (a1-a6).  on_frame(j, image, stream) is called right after
+        frame j is enqueued, on its stream (e.g. to enqueue a device->host copy); image is
+        that stream's output buffer, reused by the stream's next frame.  pre_events[j]
+        (optional pair of CUDA events) brackets frame j's ss_preprocess on its stream.  The
+        caller's current stream waits for all frames on return (no host synchronisation)."""
+        cur = torch.cuda.current_stream()
+        for st in self.streams:
+            st.wait_stream(cur)
+        for j, cam in enumerate(cams):
+            k = j % self.n_streams
+            st, rz = self.streams[k], self.rz[k]
+            with torch.cuda.stream(st):
+                e = pre_events[j] if pre_events is not None else None
+                if e is not None:
+                    e[0].record(st)
+                rz.preprocess(cam, st)
+                if e is not None:
+                    e[1].record(st)
+                rz.bin(cam, st)
+                rz.sort(st)
+                rz.render(bg, out=self.outs[k], stream=st)
+                if on_frame is not None:
+                    on_frame(j, self.outs[k], st)
+        for st in self.streams:
+            cur.wait_stream(st)
+
+
+def render_views_to_host(pipe: "FramePipeline", cams, host_out: list, bg=(0.0, 0.0, 0.0)) -> None:
     """End-to-end public call: render each camera and land its image in pinned host memory.
 
-    Frame j renders on the current stream into one of two device buffers; its device->host
-    copy runs on a side stream, overlapping frame j+1's kernels.  Returns after the last
+    Frames run on the pipeline's streams; frame j's device->host copy is enqueued on its own
+    stream right after its render (the copy engine overlaps the other streams' kernels, and the
+    stream's next frame waits for the copy before reusing the buffer).  Returns after the last
     copy completes.  host_out[j] must be pinned float32 [3, H, W] tensors."""
-    cur = torch.cuda.current_stream()
-    if not hasattr(rz, "_e2e"):
-        rz._e2e = dict(copy=torch.cuda.Stream(device=rz.device),
-                       dev=[torch.empty((3, rz.height, rz.width), dtype=torch.float32, device=rz.device)
-                            for _ in range(2)],
-                       done=[torch.cuda.Event(), torch.cuda.Event()], ready=[torch.cuda.Event(), torch.cuda.Event()])
-    st = rz._e2e
-    for j, cam in enumerate(cams):
-        b = j & 1
-        cur.wait_event(st["done"][b])            # device buffer b free again
-        rz.prepare(cam)
-        rz.render(bg, out=st["dev"][b])
-        st["ready"][b].record(cur)
-        with torch.cuda.stream(st["copy"]):
-            st["copy"].wait_event(st["ready"][b])
-            host_out[j].copy_(st["dev"][b], non_blocking=True)
-            st["done"][b].record(st["copy"])
-    st["copy"].synchronize()
+    def copy(j, img, st):
+        host_out[j].copy_(img, non_blocking=True)
+    pipe.render_views([camera_struct(c) for c in cams], bg, on_frame=copy)
+    torch.cuda.current_stream().synchronize()
 
 
 def prune_select(score: torch.Tensor, ratio: float, stream=None) -> tuple[torch.Tensor, int]:
