@@ -18,7 +18,7 @@ benchfast)
   timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-score > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench_exit=$?; tail -3 gpurun_out/${TAG}_bench.err
   python -c "import json; d=json.load(open('gpurun_out/${TAG}_bench.json')); print(d['value'], d['stages_ms'], d.get('kernels_us'))" ;;
 launches)
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --ncu --steps 1 --warmup 1 --views-per-step 2 > /dev/null 2>&1; echo ncu_launches=$?
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --ncu --no-backward --steps 1 --warmup 1 --views-per-step 2 > /dev/null 2>&1; echo ncu_launches=$?
   python profiles/summarize.py launches gpurun_out/${TAG}_launches.csv ;;
 full)
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_(preprocess|emit|render|onesweep|tile_finalize|render_backward|preprocess_backward)' -s 40 -c 12 -o gpurun_out/${TAG}_full python bench.py --ncu --steps 1 --warmup 1 --views-per-step 2 > gpurun_out/${TAG}_full.log 2>&1; echo ncu_full=$? ;;
