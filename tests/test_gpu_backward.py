@@ -124,22 +124,30 @@ def test_backward_edge_cases():
     assert float(g.abs().max()) == 0.0 and float(gr.mean_opac.abs().max()) == 0.0
 
 
-def test_fullsize_mnr360_backward_sampled():
-    """The bench workload (3.0M Gaussians, 1297x840, AccuTile), in the bench's launch
-    configuration: grad2d of 150 sampled Gaussians whose every tile is checked by the oracle
-    (their oracle sums are complete), and their parameter gradients."""
-    scene, cams = synth.make_workload("mnr360-3m")
-    cam = cams[0]
-    rz, dimg, g_gpu, T, nc = _setup(scene, cam, (0.0, 0.0, 0.0), seed=4)
+@pytest.mark.parametrize("workload,view,bg", [("mnr360-3m", 0, (0.0, 0.0, 0.0)), ("garden", 40, (0.0, 0.0, 0.0)),
+                                               ("playroom", 5, (0.1, 0.3, 0.6)), ("truck", 17, (0.0, 0.0, 0.0))])
+def test_fullsize_backward_sampled(workload, view, bg):
+    """BASELINE.json's full-size scenes (MNR360-3M = the bench workload, garden 5.8M, playroom
+    2.3M with background, truck 2.5M), AccuTile, in the bench's launch configuration: grad2d of
+    150 sampled Gaussians whose every tile is checked by the oracle (their oracle sums are
+    complete), and their parameter gradients."""
+    scene, cams = synth.make_workload(workload)
+    cam = cams[view]
+    rz, dimg, g_gpu, T, nc = _setup(scene, cam, bg, seed=4)
     P = rz.totals()["pairs"]
-    f = oracle.frame(scene, cam, "accutile", render=False, cap_hint=int(P * 1.05) + 16)
+    f = oracle.frame(scene, cam, "accutile", bg, render=False, cap_hint=int(P * 1.05) + 16)
     rng = np.random.default_rng(0)
-    vis = np.nonzero((f.counts > 0) & (f.counts <= 4))[0]
-    pick = rng.choice(vis, 150, replace=False)
+    small = (f.counts > 0) & (f.counts <= 4)
+    # most Gaussians with tiles are never blended (behind saturated pixels): sample 100 among
+    # those the GPU reports blended and 50 among all (the expected values are the oracle's)
+    blended = np.nonzero(small & np.any(g_gpu[:, :9] != 0, axis=1))[0]
+    pick = np.unique(np.concatenate([rng.choice(blended, min(100, len(blended)), replace=False),
+                                     rng.choice(np.nonzero(small)[0], 50, replace=False)]))
+    assert len(blended) >= 100
     tl = set()
     for gi in pick:
         tl.update(oracle.tiles_of_record("accutile", f.rec[gi], f.rect[gi], cam.tiles_x, cam.tiles_y).tolist())
-    g_or, gabs = oracle.render_backward(f.rec, f.values, f.ranges, cam.width, cam.height, dimg,
+    g_or, gabs = oracle.render_backward(f.rec, f.values, f.ranges, cam.width, cam.height, dimg, bg,
                                         tiles=np.array(sorted(tl), np.int32))
     d = np.abs(g_gpu[pick, :9].astype(np.float64) - g_or[pick])
     assert np.all(d <= RENDER_TOL * gabs[pick] + 1e-7), f"worst {(d / (RENDER_TOL * gabs[pick] + 1e-7)).max()}"
