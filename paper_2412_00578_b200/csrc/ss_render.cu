@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
 // (a clamped alpha passes nothing to sigma and the geometry, reading R27).  The alpha of
 // every entry is recomputed with k_render's exact operations, so the blended set is the
 // forward's.  Per batch, each warp reduces a Gaussian's 9 partials by shuffles (only when
-// one of its pixels contributes) into shared-memory accumulators; the CTA then adds each
+// one of its pixels contributes) into per-warp shared-memory slots; the CTA then adds each
 // Gaussian's sums to grad2d with three float4 atomics (one set per (tile, Gaussian)).
 __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict__ ranges,
                                                          const uint32_t *__restrict__ vals,
@@ -329,7 +329,6 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
     __shared__ float s_dC[3][256];
     __shared__ float s_Tfin[256];
     __shared__ uint32_t s_id[kBatch];
-    __shared__ uint32_t s_wmask[8][kBatch / 32];  // per warp: batch slots it wrote partials for
     __shared__ uint32_t s_warp[8];
     __shared__ uint32_t s_max;
     extern __shared__ float s_part[];              // [8 warps][kBatch][9] per-warp partial sums
@@ -370,7 +369,6 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
             const uint32_t plast = act ? st.last[pp] : 0u;
             const float Tfin = s_Tfin[pp];
             float *wpart = s_part + (size_t)warp * kBatch * 9;
-            uint32_t wm0 = 0, wm1 = 0, wm2 = 0, wm3 = 0;  // slots this warp wrote (warp-uniform)
             const float dC0 = s_dC[0][pp], dC1 = s_dC[1][pp], dC2 = s_dC[2][pp];
             float T = st.T[pp];
             float S0 = st.C0[pp], S1 = st.C1[pp], S2 = st.C2[pp];
@@ -390,7 +388,8 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
                         const float raw = cl.w * e;
                         const float alpha = fminf(0.99f, raw);  // == alpha_of(q, sigma)
                         const float om = 1.0f - alpha;
-                        const float rom = __frcp_rn(om);  // T_i = T_{i+1} / (1 - alpha_i)
+                        float rom;  // T_i = T_{i+1} / (1 - alpha_i)
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rom) : "f"(om));
                         T = T * rom;
                         const float bgs = Tfin * rom;
                         const float dLda = dC0 * (T * (cl.x - S0) - bgs * bg0) + dC1 * (T * (cl.y - S1) - bgs * bg1) +
@@ -400,14 +399,17 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
                         g[7] = dC1 * w;
                         g[8] = dC2 * w;
                         if (raw <= 0.99f) {
+                            // per pixel A = dL/dq dx, B = dL/dq dy; the CTA sums give
+                            // dL/dx2d = -2 (a SA + b SB), dL/dy2d = -2 (b SA + c SB),
+                            // dL/d(a, b, c) = (S A dx, 2 S A dy, S B dy)
                             const float dx = fpx - bx.x, dy = fpy - bx.y;
-                            const float b = 0.5f * cn.y;
                             const float dLdq = -0.5f * dLda * alpha;
-                            g[0] = -2.0f * dLdq * (cn.x * dx + b * dy);
-                            g[1] = -2.0f * dLdq * (b * dx + cn.z * dy);
-                            g[2] = dLdq * dx * dx;
-                            g[3] = 2.0f * dLdq * dx * dy;
-                            g[4] = dLdq * dy * dy;
+                            const float A = dLdq * dx, B = dLdq * dy;
+                            g[0] = A;
+                            g[1] = B;
+                            g[2] = A * dx;
+                            g[3] = A * dy;
+                            g[4] = B * dy;
                             g[5] = dLda * e;
                         }
                         S0 = alpha * cl.x + om * S0;
@@ -440,18 +442,10 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
                     for (int o = 16; o > 0; o >>= 1) v8 += __shfl_xor_sync(0xffffffffu, v8, o);
                     if ((lane & 3) == 0) wpart[k * 9 + ((lane >> 2) & 7)] = v1;
                     if (lane == 1) wpart[k * 9 + 8] = v8;
-                    const uint32_t bit = 1u << (k & 31);
-                    wm0 |= (k >> 5) == 0 ? bit : 0u;
-                    wm1 |= (k >> 5) == 1 ? bit : 0u;
-                    wm2 |= (k >> 5) == 2 ? bit : 0u;
-                    wm3 |= (k >> 5) == 3 ? bit : 0u;
+                } else {
+                    if ((lane & 3) == 0) wpart[k * 9 + ((lane >> 2) & 7)] = 0.0f;
+                    if (lane == 1) wpart[k * 9 + 8] = 0.0f;
                 }
-            }
-            if (lane == 0) {
-                s_wmask[warp][0] = wm0;
-                s_wmask[warp][1] = wm1;
-                s_wmask[warp][2] = wm2;
-                s_wmask[warp][3] = wm3;
             }
             if (act) {
                 st.T[pp] = T;
@@ -466,17 +460,20 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
             float a[9];
 #pragma unroll
             for (int f = 0; f < 9; ++f) a[f] = 0.0f;
-            bool hit = false;
             for (uint32_t w = 0; w < n_warps; ++w) {
-                if (!((s_wmask[w][k >> 5] >> (k & 31)) & 1u)) continue;
                 const float *src = s_part + ((size_t)w * kBatch + k) * 9;
 #pragma unroll
                 for (int f = 0; f < 9; ++f) a[f] += src[f];
-                hit = true;
             }
-            const float4 a0 = make_float4(a[0], a[1], a[2], a[3]);
+            const float4 cn = s.con[k];  // a, 2b, c, t of the Gaussian
+            const float b = 0.5f * cn.y;
+            const float4 a0 = make_float4(-2.0f * (cn.x * a[0] + b * a[1]), -2.0f * (b * a[0] + cn.z * a[1]), a[2],
+                                          2.0f * a[3]);
             const float4 a1 = make_float4(a[4], a[5], a[6], a[7]);
             const float a2 = a[8];
+            bool hit = false;
+#pragma unroll
+            for (int f = 0; f < 9; ++f) hit |= a[f] != 0.0f;
             if (hit) {
                 float4 *gp = grad2d + 3 * (size_t)s_id[k];
                 atomicAdd(gp + 0, a0);
