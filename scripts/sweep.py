@@ -3,7 +3,8 @@
     python scripts/sweep.py [--steps 3] [--views 32] > profiles/r01_sweep.jsonl
 
 One JSON line per (workload, mode): the forward path a1-a6 through the public API, V views
-per step, K timed steps (CUDA events, L2 flushed between steps, 2 warm-up steps), plus the
+per step with 3 frames in flight (FramePipeline), K timed steps (CUDA events, L2 flushed
+between steps, 2 warm-up steps), the single-stream per-stage split, plus the
 pruned-model regime (BASELINE config 5: U~ over every view, then the prune step removing 90%
 of the Gaussians, AccuTile).  The speed-ups of SnugBox and AccuTile over the 3-sigma baseline
 are the quantities the paper reports as 1.82x / 1.99x on an RTX A5000.
@@ -17,10 +18,10 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_2412_00578_b200 import synth  # noqa: E402
-from paper_2412_00578_b200.raster import DeviceScene, Rasterizer, camera_struct, prune  # noqa: E402
+from paper_2412_00578_b200.raster import DeviceScene, FramePipeline, Rasterizer, camera_struct, prune  # noqa: E402
 
 
-def measure(ds, cams, mode, steps, views):
+def measure(ds, cams, mode, steps, views, streams=3):
     W, H = cams[0].width, cams[0].height
     rz = Rasterizer(ds, W, H, mode=mode, capacity=max(1024, 4 * ds.n))
     vs = list(range(0, len(cams), max(1, len(cams) // views)))[:views]
@@ -35,21 +36,36 @@ def measure(ds, cams, mode, steps, views):
     out = torch.empty((3, H, W), dtype=torch.float32, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
+    pipe = FramePipeline(ds, W, H, mode=mode, n_streams=streams, capacity=rz.capacity)
     ms = []
     for k in range(steps + 2):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
-        for c in cs:
-            rz.prepare(c)
-            rz.render(out=out)
+        pipe.render_views(cs)
         b.record(st)
         torch.cuda.synchronize()
         if k >= 2:
             ms.append(a.elapsed_time(b))
-    del rz
+    # per-stage split, single stream (events around each call)
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in cs]
+    flush.zero_()
+    for c, e in zip(cs, ev):
+        e[0].record(st)
+        rz.preprocess(c)
+        e[1].record(st)
+        rz.bin(c)
+        e[2].record(st)
+        rz.sort()
+        e[3].record(st)
+        rz.render(out=out)
+        e[4].record(st)
+    torch.cuda.synchronize()
+    stages = {s_: float(np.mean([e[i].elapsed_time(e[i + 1]) for e in ev]))
+              for i, s_ in enumerate(["preprocess", "bin", "sort", "render"])}
+    del rz, pipe
     return {"fps": len(cs) * len(ms) / (sum(ms) / 1e3), "pairs_per_frame": float(np.mean(pairs)),
-            "views": len(cs), "steps": len(ms)}
+            "views": len(cs), "steps": len(ms), "frames_in_flight": streams, "stages_ms_single_stream": stages}
 
 
 def main():
