@@ -165,17 +165,17 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------------------ ours (GPU)
-def stage_bytes(stage, N, n_vis, P, n_tiles, W, H, sh_floats):
+def stage_bytes(stage, N, n_vis, P, n_tiles, W, H, sh_floats, n_col=0):
     """Algorithmic bytes per launch: what the step must move at minimum."""
-    if stage == "preprocess":
-        return 16 * N + (32 + 4 * sh_floats) * n_vis + 48 * n_vis + 4 * N
+    if stage == "preprocess":   # mean + depth key of every Gaussian; scale, rot and record of the
+        return 16 * N + 32 * n_vis + 48 * n_vis + 4 * N      # visible (colours deferred to the render)
     if stage == "bin":       # depth order (4 passes: key + value read and written), entry scan,
         # level 1 (order + emission record per visible Gaussian, entries written: E <= P / 2), level 2 count
         return 4 * N + 4 * 16 * n_vis + 8 * n_vis + (4 + 32) * n_vis + 8 * (P // 2) + 8 * n_tiles
     if stage == "sort":      # level 2 write: read the entries, one id per pair
         return 8 * (P // 2) + 4 * P
-    if stage == "render":    # id + gathered record (36 B used) per pair, image
-        return 40 * P + 12 * W * H
+    if stage == "render":    # id + gathered record (36 B used) per pair, image, and the lazy colours:
+        return 40 * P + 12 * W * H + n_col * (16 + 4 * sh_floats)   # mean + SH read, q2 written
     raise KeyError(stage)
 
 
@@ -213,7 +213,7 @@ def run_ours(args):
         rz = Rasterizer(ds, W, H, mode=args.mode, capacity=max(1024, 8 * ds.n))
 
     # sizing + per-view statistics (untimed): pairs per frame, visible counts, render work
-    pairs, nvis, E_pix, E_blend, E_cta, E_kept = {}, {}, {}, {}, {}, {}
+    pairs, nvis, E_pix, E_blend, E_cta, E_kept, ncol = {}, {}, {}, {}, {}, {}, {}
     for v in my_views:
         rz.ensure_capacity(cams[v])
     cap = rz.capacity
@@ -223,6 +223,7 @@ def run_ours(args):
         t = rz.totals()
         assert not t["overflow"]
         pairs[v], nvis[v] = t["pairs"], t["n_visible"]
+        ncol[v] = int(((rz.records()[:, 8] == 1.0) & (rz.depth_keys() != -1)).sum().item())
         st = rz.render_stats()
         E_pix[v], E_blend[v], E_cta[v], E_kept[v] = st["E_pix"], st["E_blend"], st["E_cta"], st["E_kept"]
     # shrink capacity to the measured maximum (+2%) so the per-frame memset is tight
@@ -319,10 +320,10 @@ def run_ours(args):
             ach = flops / (stage_ms[s] / 1e3) / 1e12
             stage_info[s] = {"ms": stage_ms[s], "bound": "alu", "achieved": ach, "peak": fp32_peak,
                              "unit": "TFLOP/s", "frac": ach / fp32_peak,
-                             "gbs_algorithmic": stage_bytes(s, ds.n, NVm, Pm, rz.n_tiles, W, H, sh_floats)
+                             "gbs_algorithmic": stage_bytes(s, ds.n, NVm, Pm, rz.n_tiles, W, H, sh_floats, mean(ncol))
                              / (stage_ms[s] / 1e3) / 1e9}
         else:
-            b = stage_bytes(s, ds.n, NVm, Pm, rz.n_tiles, W, H, sh_floats)
+            b = stage_bytes(s, ds.n, NVm, Pm, rz.n_tiles, W, H, sh_floats, mean(ncol))
             ach = b / (stage_ms[s] / 1e3) / 1e9
             stage_info[s] = {"ms": stage_ms[s], "bound": "hbm", "achieved": ach, "peak": hbm_peak,
                              "unit": "GB/s", "frac": ach / hbm_peak, "bytes": b}
@@ -527,6 +528,7 @@ def run_ours(args):
             "pairs_per_frame": {"mean": Pm, "min": min(pairs.values()), "max": max(pairs.values())},
             "pairs_per_s": value * Pm,
             "visible_per_frame": NVm,
+            "coloured_per_frame": mean(ncol),
             "stages_ms": {s: stage_ms[s] for s in stages},
             "host_enqueue_ms_per_frame": host_ms,
             "stages": stage_info,

@@ -104,8 +104,12 @@ typedef struct {
 
 /* Byte offsets of every sub-buffer inside the workspace (for inspection and tests).
  * Records of a Gaussian with >= 1 tile (written only for those):
- *   rec  (48 B, render): q0 = (x2d, y2d, a, b), q1 = (c, t, sigma, 0), q2 = (0, r, g, b)
- *        (a, b, c) = conic Sigma_2D^-1 (Eq. 10); t = 2 log(255 sigma) (Eq. 11)
+ *   rec  (48 B, render): q0 = (x2d, y2d, a, b), q1 = (c, t, sigma, 0), q2 = (f, r, g, b)
+ *        (a, b, c) = conic Sigma_2D^-1 (Eq. 10); t = 2 log(255 sigma) (Eq. 11); the colour
+ *        (R13) is computed lazily: ss_preprocess writes q2 = 0 (f = 0, pending) and the first
+ *        render-path call that gathers the record (ss_render, ss_prune_score,
+ *        ss_render_backward, ss_render_stats) computes it from the scene's SH and stores
+ *        q2 = (1, r, g, b); ss_finalize_colours completes the rest (inspection)
  *   erec (32 B, emission, one sector): (count, info, p0..p5); the payload holds the
  *        non-empty line spans (tmin | tmax << 9 | line << 18) of an AccuTile set of at most 6
  *        lines, or up to 6 super-tile entries (super-tile id | mask of its 4x4 tiles << 16,
@@ -173,6 +177,11 @@ SS_API ss_status ss_sorted_keys(const ss_frame *frame /*host*/, uint64_t *keys, 
  * including the last blended one) are optional (NULL). bg is host float[3]. */
 SS_API ss_status ss_render(const ss_frame *frame /*host*/, const float *bg /*host [3]*/, float *out_rgb,
                     float *out_T, uint32_t *out_ncontrib, void *stream);
+
+/* Inspection: compute the colour of every record still pending (Gaussians with tiles that no
+ * render-path call has gathered), so that rec holds all colours.  Requires ss_preprocess on
+ * the frame; the scene passed to it must still be alive. */
+SS_API ss_status ss_finalize_colours(const ss_frame *frame /*host*/, void *stream);
 
 /* Measurement helper (never on the timed path): work counts of ss_render for the frame,
  * accumulated into counters (device uint64 [5]): E_pix (per-pixel evaluations until each

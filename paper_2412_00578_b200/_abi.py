@@ -13,7 +13,7 @@ SS_OK, SS_ERR_INVALID_ARG, SS_ERR_CAPACITY, SS_ERR_CUDA, SS_ERR_UNSUPPORTED = ra
 MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}
 
 EXPORTS = ["ss_frame_workspace_size", "ss_frame_layout", "ss_preprocess", "ss_bin", "ss_sort", "ss_sorted_keys",
-           "ss_render", "ss_render_stats", "ss_prune_score", "ss_render_frame",
+           "ss_render", "ss_render_stats", "ss_finalize_colours", "ss_prune_score", "ss_render_frame",
            "ss_prune_workspace_size", "ss_prune_count", "ss_prune_select", "ss_compact_scene",
            "ss_render_backward", "ss_preprocess_backward", "ss_l1_loss_grad", "ss_adam_init", "ss_adam_step", "ss_status_string", "ss_last_cuda_error", "ss_version"]
 
@@ -69,6 +69,7 @@ def lib() -> C.CDLL:
             "ss_sorted_keys": (st, [P(SsFrame), vp, vp]),
             "ss_render": (st, [P(SsFrame), P(C.c_float), vp, vp, vp, vp]),
             "ss_render_stats": (st, [P(SsFrame), vp, vp]),
+            "ss_finalize_colours": (st, [P(SsFrame), vp]),
             "ss_prune_score": (st, [P(SsFrame), P(C.c_float), vp, vp]),
             "ss_render_frame": (st, [P(SsScene), P(SsCamera), st, P(SsFrame), P(C.c_float), vp, vp, vp, vp]),
             "ss_prune_workspace_size": (C.c_size_t, [C.c_int32]),

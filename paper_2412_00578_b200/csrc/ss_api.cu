@@ -61,6 +61,7 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     P.ranges = take(8 * T);
     P.tile_count = take(4 * T);
     L->tile_base = take(4 * T);
+    L->color_src = take(64);
     P.overflow = take(4);
     // ---- regions each call clears for itself (so every call is idempotent given its inputs)
     L->zero_pre = off;  // written by ss_preprocess
@@ -192,6 +193,13 @@ ss_status ss_render(const ss_frame *frame, const float *bg, float *out_rgb, floa
     if (!bg || !out_rgb) return SS_ERR_INVALID_ARG;
     return cuda_status(launch_render(frame->ws, L, frame->width, frame->height, bg[0], bg[1], bg[2], out_rgb, out_T,
                                      out_ncontrib, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_finalize_colours(const ss_frame *frame, void *stream) {
+    Layout L;
+    ss_status s = check_frame(frame, &L);
+    if (s != SS_OK) return s;
+    return cuda_status(launch_finalize_colours(frame->ws, L, static_cast<cudaStream_t>(stream)));
 }
 
 ss_status ss_render_stats(const ss_frame *frame, uint64_t *counters, void *stream) {

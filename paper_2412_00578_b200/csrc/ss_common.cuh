@@ -62,6 +62,7 @@ struct Layout {
     size_t l2_blocks;               // uint2 [l2_max_blocks] (super-tile, first entry) of each block
     size_t l2_BC;                   // uint32 [l2_max_blocks][16] pairs per (block, tile) -> prefix
     size_t tile_base;               // uint32 [n_tiles] first sorted position of each tile
+    size_t color_src;               // ColorSrc (64 B): scene mean / SH pointers + camera centre of the frame
     size_t zero_pre, zero_pre_end;  // regions each call clears for itself
     size_t zero_bin, zero_bin_end;
     size_t hist_depth;              // uint32 [4][256]
@@ -144,6 +145,7 @@ cudaError_t launch_tile_write(void *ws, const Layout &L, cudaStream_t st);
 cudaError_t launch_sorted_keys(void *ws, const Layout &L, uint64_t *keys, cudaStream_t st);
 cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2, float *out_rgb,
                           float *out_T, uint32_t *out_nc, cudaStream_t st);
+cudaError_t launch_finalize_colours(void *ws, const Layout &L, cudaStream_t st);
 cudaError_t launch_render_stats(void *ws, const Layout &L, int W, int H, unsigned long long *counters,
                                 cudaStream_t st);
 cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2,

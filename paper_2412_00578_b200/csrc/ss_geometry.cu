@@ -8,38 +8,11 @@
 // function on the same values (R1) and are exact for the stored conic.
 //
 // P:n = /root/reference/PAPER.md line n.
-#include <cuda_pipeline.h>
-
+#include "ss_color.cuh"
 #include "ss_tilegeom.cuh"
 
 namespace ss {
 namespace {
-
-// ---------------------------------------------------------------- SH basis (R13)
-template <int DEG>
-__device__ __forceinline__ void sh_basis(float x, float y, float z, float *Y) {
-    Y[0] = 0.28209479177387814f;
-    if (DEG < 1) return;
-    const float C1 = 0.4886025119029199f;
-    Y[1] = -C1 * y;
-    Y[2] = C1 * z;
-    Y[3] = -C1 * x;
-    if (DEG < 2) return;
-    const float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
-    Y[4] = 1.0925484305920792f * xy;
-    Y[5] = -1.0925484305920792f * yz;
-    Y[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
-    Y[7] = -1.0925484305920792f * xz;
-    Y[8] = 0.5462742152960396f * (xx - yy);
-    if (DEG < 3) return;
-    Y[9] = -0.5900435899266435f * y * (3.0f * xx - yy);
-    Y[10] = 2.890611442640554f * xy * z;
-    Y[11] = -0.4570457994644658f * y * (4.0f * zz - xx - yy);
-    Y[12] = 0.3731763325901154f * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
-    Y[13] = -0.4570457994644658f * x * (4.0f * zz - xx - yy);
-    Y[14] = 1.445305721320277f * z * (xx - yy);
-    Y[15] = -0.5900435899266435f * x * (xx - 3.0f * yy);
-}
 
 // ---------------------------------------------------------------- a1 preprocess kernel
 constexpr int kPreThreads = 256;  // CTA size
@@ -54,23 +27,21 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
                                                     uint32_t *__restrict__ depth_key, uint32_t *__restrict__ gne,
                                                     uint32_t *__restrict__ hist,
                                                     uint32_t *__restrict__ n_visible,
-                                                    uint32_t *__restrict__ total_pairs) {
+                                                    uint32_t *__restrict__ total_pairs, ColorSrc cs_in,
+                                                    ColorSrc *__restrict__ cs_out) {
     pdl_enter();
+    if (blockIdx.x == 0 && threadIdx.x == 0) *cs_out = cs_in;  // the render path's lazy colour source
     __shared__ uint32_t s_hist[kDepthPasses][256];
     __shared__ uint32_t s_vis, s_pairs;
     for (int k = threadIdx.x; k < kDepthPasses * 256; k += blockDim.x) (&s_hist[0][0])[k] = 0;
     if (threadIdx.x == 0) s_vis = s_pairs = 0;
     __syncthreads();
-    constexpr int NB = (DEG + 1) * (DEG + 1);
-    constexpr int NP = (NB * 3 + 3) / 4;
     uint32_t my_vis = 0, my_pairs = 0;
     // camera constants of the J clamp (R5), the same values the per-Gaussian form would give
     const float limx = cam.clip * ((0.5f * (float)cam.W) / cam.fx);
     const float limy = cam.clip * ((0.5f * (float)cam.H) / cam.fy);
     const int stx = (cam.tiles_x + kSuper - 1) / kSuper;
     const int lane = threadIdx.x & 31;
-    extern __shared__ float4 s_sh[];                  // per thread: one SH block (+1 float4 pad)
-    float4 *my_sh = s_sh + (size_t)threadIdx.x * (NP + 1);
     // warp-uniform grid-stride loop (the tall-Gaussian phase below is warp-collective)
     for (int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += gridDim.x * blockDim.x) {
         const int i = i0 + lane;
@@ -82,7 +53,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
         const float px = cam.V[0] * mo.x + cam.V[1] * mo.y + cam.V[2] * mo.z + cam.V[3];
         const float py = cam.V[4] * mo.x + cam.V[5] * mo.y + cam.V[6] * mo.z + cam.V[7];
         const float pz = cam.V[8] * mo.x + cam.V[9] * mo.y + cam.V[10] * mo.z + cam.V[11];
-        float x2d = 0.f, y2d = 0.f, a = 0.f, b = 0.f, c = 0.f, rgb0 = 0.f, rgb1 = 0.f, rgb2 = 0.f;
+        float x2d = 0.f, y2d = 0.f, a = 0.f, b = 0.f, c = 0.f;
         double td = 0.0;
         int4 R = make_int4(0, 0, 0, 0);
         Snug snug;
@@ -159,13 +130,6 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
                                         cam.tiles_y);
                     } else {
                         R = rect_of_snug(snug, cam.tiles_x, cam.tiles_y);
-                    }
-                    if (R.x < R.y && R.z < R.w) {
-                        // the Gaussian has (almost surely) tiles: its SH block is copied to shared
-                        // memory now (cp.async), overlapping the tile sweep below
-#pragma unroll
-                        for (int p = 0; p < NP; ++p) __pipeline_memcpy_async(my_sh + p, sh + (size_t)i * NP + p, 16);
-                        __pipeline_commit();
                     }
                     if (mode == SS_BIN_ACCUTILE) {
                         Sweep w;
@@ -257,40 +221,13 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
             }
         }
         if (count > 0) {
-            // colour (R13): only Gaussians with tiles read their SH planes
-            const float dx = mo.x - cam.cpx, dy = mo.y - cam.cpy, dz = mo.z - cam.cpz;
-            const float len = sqrtf(dx * dx + dy * dy + dz * dz);
-            const float il = 1.0f / len;
-            float Y[16];
-            sh_basis<DEG>(dx * il, dy * il, dz * il, Y);
-            float hc[NP * 4];
-            __pipeline_wait_prior(0);  // the SH block copied before the tile sweep
-#pragma unroll
-            for (int p = 0; p < NP; ++p) {
-                const float4 v = my_sh[p];
-                hc[4 * p + 0] = v.x;
-                hc[4 * p + 1] = v.y;
-                hc[4 * p + 2] = v.z;
-                hc[4 * p + 3] = v.w;
-            }
-            float acc0 = 0.0f, acc1 = 0.0f, acc2 = 0.0f;
-#pragma unroll
-            for (int k = 0; k < NB; ++k) {
-                acc0 = acc0 + Y[k] * hc[3 * k + 0];
-                acc1 = acc1 + Y[k] * hc[3 * k + 1];
-                acc2 = acc2 + Y[k] * hc[3 * k + 2];
-            }
-            acc0 = acc0 + 0.5f;
-            acc1 = acc1 + 0.5f;
-            acc2 = acc2 + 0.5f;
-            rgb0 = acc0 > 0.0f ? acc0 : 0.0f;
-            rgb1 = acc1 > 0.0f ? acc1 : 0.0f;
-            rgb2 = acc2 > 0.0f ? acc2 : 0.0f;
-            // render record (48 B): q0 (x, y, a, b) | q1 (c, t, sigma, 0) | q2 (0, r, g, b)
+            // render record (48 B): q0 (x, y, a, b) | q1 (c, t, sigma, 0) | q2 (colour flag, r, g, b);
+            // the colour (R13) is left pending (flag 0) and computed by the first render-path
+            // kernel that gathers the record (ss_color.cuh)
             float4 *q = rec + 3 * (size_t)i;
             q[0] = make_float4(x2d, y2d, a, b);
             q[1] = make_float4(c, (float)td, mo.w, 0.0f);
-            q[2] = make_float4(0.0f, rgb0, rgb1, rgb2);
+            q[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
             // emission record (32 B, one sector): (count, info, p0..p5); the payload p holds the
             // non-empty line spans of an AccuTile set of at most kLaneRows lines (tmin | tmax << 9
             // | line << 18), or up to kInlineEnt super-tile entries (super-tile | mask << 16), or
@@ -322,7 +259,6 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess(int n, c
             ++my_vis;
             my_pairs += count;
         } else if (valid) {
-            __pipeline_wait_prior(0);  // a copy issued for a Gaussian that ended without tiles
             depth_key[i] = kNoTiles;
             gne[i] = 0u;
         }
@@ -362,9 +298,16 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
     sc.n, reinterpret_cast<const float4 *>(sc.mean_opac), reinterpret_cast<const float4 *>(sc.scale),         \
         reinterpret_cast<const float4 *>(sc.rot), reinterpret_cast<const float4 *>(sc.sh), cam, mode,         \
         at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key), at<uint32_t>(ws, L.gne), \
-        at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs)
-    const int NPd = ((sc.sh_degree + 1) * (sc.sh_degree + 1) * 3 + 3) / 4;
-    const size_t smem = (size_t)kPreThreads * (NPd + 1) * 16;  // per-thread SH staging (cp.async)
+        at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs), csrc,        \
+        at<ColorSrc>(ws, L.color_src)
+    ColorSrc csrc;
+    csrc.mean_opac = reinterpret_cast<const float4 *>(sc.mean_opac);
+    csrc.sh = reinterpret_cast<const float4 *>(sc.sh);
+    csrc.cpx = cam.cpx;
+    csrc.cpy = cam.cpy;
+    csrc.cpz = cam.cpz;
+    csrc.deg = sc.sh_degree;
+    const size_t smem = 0;
     static int done[4][64] = {{0}};
     cudaError_t e = cudaSuccess;
     switch (sc.sh_degree) {

@@ -10,7 +10,7 @@
 // uses the pinned chain u = fma(a, dx, (2b) dy); q = fma(dx, u, (c dy) dy) with explicit
 // round-to-nearest intrinsics, so it is bit-identical to the oracle's; alpha uses the SFU
 // exp2 (ex2.approx), which the image tolerance (1e-4) covers.
-#include "ss_common.cuh"
+#include "ss_color.cuh"
 
 namespace ss {
 namespace {
@@ -41,12 +41,12 @@ __device__ __forceinline__ float alpha_of(float q, float sigma) {
 
 __device__ __forceinline__ void load_batch(Batch &s, const uint32_t *__restrict__ vals,
                                            const float4 *__restrict__ rec, uint32_t j, uint32_t end,
-                                           uint32_t *s_id) {
+                                           uint32_t *s_id, const ColorSrc &cs) {
     if (threadIdx.x < kBatch && j < end) {
         const uint32_t g = vals[j];
         const float4 q0 = __ldg(rec + 3 * (size_t)g + 0);  // x, y, a, b
-        const float4 q1 = __ldg(rec + 3 * (size_t)g + 1);  // c, t, sigma, hx
-        const float4 q2 = __ldg(rec + 3 * (size_t)g + 2);  // hy, r, g, b
+        const float4 q1 = __ldg(rec + 3 * (size_t)g + 1);  // c, t, sigma, 0
+        const float4 q2 = record_colour(rec, g, cs);        // done flag, r, g, b (lazy colour)
         s.box[threadIdx.x] = make_float4(q0.x, q0.y, 0.0f, 0.0f);
         s.con[threadIdx.x] = make_float4(q0.z, q0.w + q0.w, q1.x, q1.y);
         s.col[threadIdx.x] = make_float4(q2.y, q2.z, q2.w, q1.z);
@@ -86,11 +86,13 @@ __device__ __forceinline__ uint32_t compact_active(bool active, PixState &st, ui
 }
 
 template <bool NC>  // NC: track the last blended list entry per pixel (out_ncontrib requested)
-__global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
+__global__ void __launch_bounds__(256, 6) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
                                                 const float4 *__restrict__ rec, int W, int H, int tiles_x, float bg0,
                                                 float bg1, float bg2, float *__restrict__ out_rgb,
-                                                float *__restrict__ out_T, uint32_t *__restrict__ out_nc) {
+                                                float *__restrict__ out_T, uint32_t *__restrict__ out_nc,
+        const ColorSrc *__restrict__ csp) {
     pdl_enter();
+    const ColorSrc cs = *csp;
     __shared__ Batch s;
     __shared__ PixState st;
     __shared__ uint32_t s_warp[8];
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
         __syncthreads();
         const uint32_t n_active = compact_active(!st.done[threadIdx.x], st, s_warp);
         if (n_active == 0) break;
-        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr);
+        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr, cs);
         __syncthreads();
         if (threadIdx.x < n_active) {
             const int pp = st.list[threadIdx.x];
@@ -175,8 +177,10 @@ __global__ void __launch_bounds__(256) k_render(const uint2 *__restrict__ ranges
 __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ ranges,
                                                      const uint32_t *__restrict__ vals,
                                                      const float4 *__restrict__ rec, int W, int H, int tiles_x,
-                                                     float bg0, float bg1, float bg2, double *__restrict__ score) {
+                                                     float bg0, float bg1, float bg2, double *__restrict__ score,
+        const ColorSrc *__restrict__ csp) {
     pdl_enter();
+    const ColorSrc cs = *csp;
     __shared__ Batch s;
     __shared__ PixState st;  // forward: T, last, done; backward: T (running), C0..2 = suffix S
     __shared__ float s_Tfin[256];
@@ -199,7 +203,7 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
         __syncthreads();
         const uint32_t n_active = compact_active(!st.done[threadIdx.x], st, s_warp);
         if (n_active == 0) break;
-        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr);
+        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr, cs);
         __syncthreads();
         if (threadIdx.x < n_active) {
             const int pp = st.list[threadIdx.x];
@@ -244,7 +248,7 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
         const int cnt = (int)(end - start);
         __syncthreads();
         const uint32_t n_active = compact_active(my_last > start - range.x, st, s_warp);
-        load_batch(s, vals, rec, start + threadIdx.x, end, s_id);
+        load_batch(s, vals, rec, start + threadIdx.x, end, s_id, cs);
         __syncthreads();
         const uint32_t n_warps = (n_active + 31) / 32;
         if ((uint32_t)warp < n_warps) {
@@ -322,8 +326,10 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
                                                          const float *__restrict__ dimg,
                                                          const float *__restrict__ T_final,
                                                          const uint32_t *__restrict__ n_contrib,
-                                                         float4 *__restrict__ grad2d) {
+                                                         float4 *__restrict__ grad2d,
+        const ColorSrc *__restrict__ csp) {
     pdl_enter();
+    const ColorSrc cs = *csp;
     __shared__ Batch s;
     __shared__ PixState st;  // T (running), C0..2 = suffix S, last = n_contrib
     __shared__ float s_dC[3][256];
@@ -356,7 +362,7 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
         const int cnt = (int)(end - start);
         __syncthreads();
         const uint32_t n_active = compact_active(my_last > start - range.x, st, s_warp);
-        load_batch(s, vals, rec, start + threadIdx.x, end, s_id);
+        load_batch(s, vals, rec, start + threadIdx.x, end, s_id, cs);
         __syncthreads();
         const uint32_t n_warps = (n_active + 31) / 32;
         const int warp = threadIdx.x >> 5;
@@ -493,7 +499,9 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
 __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ ranges,
                                                       const uint32_t *__restrict__ vals,
                                                       const float4 *__restrict__ rec, int W, int H, int tiles_x,
-                                                      unsigned long long *counters) {
+                                                      unsigned long long *counters,
+        const ColorSrc *__restrict__ csp) {
+    const ColorSrc cs = *csp;
     __shared__ Batch s;
     __shared__ unsigned long long s_acc[5];
     const int tile = blockIdx.x;
@@ -508,7 +516,7 @@ __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ 
     if (threadIdx.x < 5) s_acc[threadIdx.x] = 0;
     for (uint32_t start = range.x; start < range.y; start += kBatch) {
         if (__syncthreads_count(done) == blockDim.x) break;
-        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr);
+        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr, cs);
         __syncthreads();
         const int cnt = min((uint32_t)kBatch, range.y - start);
         e_cta += cnt;
@@ -552,12 +560,30 @@ __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ 
 
 }  // namespace
 
+namespace {
+// Colours still pending after the frame's kernels (Gaussians no tile reached): inspection only.
+__global__ void __launch_bounds__(256) k_finalize_colours(int n, const uint32_t *__restrict__ depth_key,
+                                                          const float4 *rec, const ColorSrc *__restrict__ csp) {
+    pdl_enter();
+    const ColorSrc cs = *csp;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && depth_key[i] != kNoTiles) record_colour(rec, (uint32_t)i, cs);
+}
+}  // namespace
+
+cudaError_t launch_finalize_colours(void *ws, const Layout &L, cudaStream_t st) {
+    if (L.n == 0) return cudaSuccess;
+    launch_pdl(k_finalize_colours, (L.n + 255) / 256, 256, 0, st, (int)L.n, at<const uint32_t>(ws, L.pub.depth_key),
+               at<const float4>(ws, L.pub.rec), at<const ColorSrc>(ws, L.color_src));
+    return cudaGetLastError();
+}
+
 cudaError_t launch_render_stats(void *ws, const Layout &L, int W, int H, unsigned long long *counters,
                                 cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
     k_render_stats<<<P.n_tiles, 256, 0, st>>>(at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
-                                               at<const float4>(ws, P.rec), W, H, P.tiles_x, counters);
+                                               at<const float4>(ws, P.rec), W, H, P.tiles_x, counters, at<const ColorSrc>(ws, L.color_src));
     return cudaGetLastError();
 }
 
@@ -568,11 +594,11 @@ cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, fl
     if (out_nc)
         launch_pdl(k_render<true>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
                                                    at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
-                                                   out_T, out_nc);
+                                                   out_T, out_nc, at<const ColorSrc>(ws, L.color_src));
     else
         launch_pdl(k_render<false>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
                                                     at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
-                                                    out_T, out_nc);
+                                                    out_T, out_nc, at<const ColorSrc>(ws, L.color_src));
     return cudaGetLastError();
 }
 
@@ -587,7 +613,7 @@ cudaError_t launch_render_backward(void *ws, const Layout &L, int W, int H, floa
     if (e != cudaSuccess) return e;
     launch_pdl(k_render_backward, P.n_tiles, 256, smem, st, at<const uint2>(ws, P.ranges),
                at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
-               dimg, T_final, n_contrib, reinterpret_cast<float4 *>(grad2d));
+               dimg, T_final, n_contrib, reinterpret_cast<float4 *>(grad2d), at<const ColorSrc>(ws, L.color_src));
     return cudaGetLastError();
 }
 
@@ -596,7 +622,8 @@ cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
     launch_pdl(k_prune_score, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
-                                              at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, score);
+                                              at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, score,
+                                              at<const ColorSrc>(ws, L.color_src));
     return cudaGetLastError();
 }
 

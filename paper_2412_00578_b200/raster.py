@@ -104,8 +104,9 @@ class Rasterizer:
 
     # views of the intermediates (zero-copy)
     def records(self) -> torch.Tensor:
-        """[N, 12] float32 render records: (x, y, a, b | c, t, sigma, 0 | 0, r, g, b); valid
-        only where depth_keys() != 0xFFFFFFFF."""
+        """[N, 12] float32 render records: (x, y, a, b | c, t, sigma, 0 | f, r, g, b); valid
+        only where depth_keys() != 0xFFFFFFFF; the colour only where f = 1 (call
+        finalize_colours() first to complete them all)."""
         return self._view(self.layout.rec, 12 * self.scene.n, torch.float32).view(self.scene.n, 12)
 
     def emit_records(self) -> torch.Tensor:
@@ -173,6 +174,12 @@ class Rasterizer:
         if want_T or want_ncontrib:
             return out, T, nc
         return out
+
+    def finalize_colours(self, stream=None) -> None:
+        """Compute every record colour still pending (inspection; the render path computes the
+        colours it needs lazily)."""
+        check(lib().ss_finalize_colours(C.byref(self.frame), C.c_void_p(_stream_handle(stream))),
+              "ss_finalize_colours")
 
     def render_stats(self, stream=None) -> dict:
         """Work counts of the render for the current frame (measurement; synchronises)."""

@@ -28,6 +28,7 @@ def _rz(scene, cam, mode, capacity=None):
 def _gpu_frame(scene, cam, mode, bg=(0.0, 0.0, 0.0), capacity=None):
     rz = _rz(scene, cam, mode, capacity)
     img, T, nc = rz.render_frame(cam, bg, want_T=True, want_ncontrib=True)
+    rz.finalize_colours()   # colours the render did not need (never gathered) are still pending
     torch.cuda.synchronize()
     tot = rz.totals()
     P = tot["pairs"]
@@ -53,6 +54,7 @@ def _check_frame(scene, cam, mode, bg=(0.0, 0.0, 0.0), capacity=None, image=True
     vis = cnt > 0
     # records (bit-exact): GPU (x,y,a,b | c,t,sigma,hx | hy,r,g,b); oracle (x,y,depth,a,b,c,sigma,t,r,g,b,vis)
     gr, orr = g["rec"][vis], f.rec[vis]
+    assert np.all(gr[:, 8] == 1.0), "colour flags"   # every colour computed (lazily or by finalize)
     pairs = [(0, 0), (1, 1), (2, 3), (3, 4), (4, 5), (5, 7), (6, 6), (9, 8), (10, 9), (11, 10)]
     for gi, oi in pairs:
         assert np.array_equal(gr[:, gi].view(np.uint32), orr[:, oi].view(np.uint32)), f"record field {gi}"
