@@ -32,6 +32,16 @@ sys.path.insert(0, ROOT)
 FP32_LANES_PER_SM = 128  # B200: 4 SMSPs x 32 FP32 lanes (FFMA = 2 flop)
 
 
+METRIC = ("rendered frames/sec (forward a1-a6) & Gaussian-tile pairs/frame, "
+          "3M-Gaussian MipNeRF360-shaped")
+
+
+def base_config(args, n, W, H, sh_degree, views):
+    """The config keys both arms report (the reference arm runs the same workload)."""
+    return {"workload": args.workload, "n_gaussians": n, "width": W, "height": H, "views": views,
+            "mode": args.mode, "sh_degree": sh_degree}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -132,8 +142,10 @@ def run_oracle_steps(name, mode, steps, warmup, workers):
     pool.close()
     pool.join()
     total = sum(times)
+    sc, cams = _POOL_SCENE
     return {"value": steps * workers / total, "ms_per_step": 1e3 * total / steps, "pairs": pairs,
-            "frames": steps * workers}
+            "frames": steps * workers, "n": sc.n, "W": cams[0].width, "H": cams[0].height,
+            "sh_degree": sc.sh_degree, "views": len(cams)}
 
 
 def host_cores() -> int:
@@ -150,10 +162,12 @@ def run_reference(args):
     workers = max(1, min(8, host_cores()))
     r = run_oracle_steps(args.workload, args.mode, args.steps, args.warmup, workers)
     line = {
-        "impl": "reference", "metric": "rendered frames/sec (forward a1-a6)", "value": r["value"],
+        "impl": "reference", "metric": METRIC, "value": r["value"],
         "unit": "frames/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic", "config": {"workload": args.workload, "mode": args.mode},
+        "dtype": "f32", "data": "synthetic",
+        "config": {**base_config(args, r["n"], r["W"], r["H"], r["sh_degree"], r["views"]),
+                   "parallelism": "CPU oracle, one view per worker process"},
         "pairs_per_frame": statistics.mean(r["pairs"]) if r["pairs"] else None,
         "cpu_baseline": {"value": r["value"], "unit": "frames/s", "cores": workers, "kind": "oracle",
                          "sample": f"{r['frames']} full views of {args.workload} ({workers} worker processes, "
@@ -513,8 +527,7 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": "rendered frames/sec (forward a1-a6) & Gaussian-tile pairs/frame, "
-                      "3M-Gaussian MipNeRF360-shaped",
+            "metric": METRIC,
             "value": value, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
