@@ -379,17 +379,14 @@ def run_ours(args):
     if not args.no_score and not args.ncu:
         score = torch.zeros(ds.n, dtype=torch.float64, device=dev)
         n_sv = min(len(my_views), 2 * V)
-        for v in my_views[:4]:
-            rz.prepare(cams[v])
-            rz.prune_score(score)
+        svs = [cstructs[v] if v in cstructs else camera_struct(cams[v]) for v in my_views[:n_sv]]
+        pipe.score_views(svs[:4], score)
         score.zero_()
         dist.barrier()
         torch.cuda.synchronize()
         a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         a.record(stream)
-        for v in my_views[:n_sv]:
-            rz.prepare(cams[v])
-            rz.prune_score(score)
+        pipe.score_views(svs, score)       # a1-a5 + a7 per view, frames in flight
         b.record(stream)
         dist.allreduce_scores(score)
         c.record(stream)
@@ -397,7 +394,8 @@ def run_ours(args):
         ms_s = dist.max_over_ranks(a.elapsed_time(c))
         score_info = {"views_per_s": world * n_sv / (ms_s / 1e3), "views": world * n_sv,
                       "ms_score_views": a.elapsed_time(b), "ms_allreduce": b.elapsed_time(c),
-                      "allreduce_bytes": 8 * ds.n, "dtype": "f64 accumulate, f32 per-pixel"}
+                      "allreduce_bytes": 8 * ds.n, "dtype": "f64 accumulate, f32 per-pixel",
+                      "frames_in_flight": args.streams}
 
     # ---- backward pass (NEXT-2): forward with T / n_contrib, render backward, preprocess backward
     bw_info = None

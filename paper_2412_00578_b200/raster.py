@@ -315,6 +315,25 @@ class FramePipeline:
             cur.wait_stream(st)
 
 
+    def score_views(self, cams, score: torch.Tensor, bg=(0.0, 0.0, 0.0)) -> torch.Tensor:
+        """a1-a5 + a7 for every camera, the frames in flight on the pipeline's streams, all
+        adding into the one float64 score vector (device atomics; no host synchronisation).
+        The caller's current stream waits for all frames on return."""
+        assert score.dtype == torch.float64 and score.is_cuda
+        cur = torch.cuda.current_stream()
+        for st in self.streams:
+            st.wait_stream(cur)
+        for j, cam in enumerate(cams):
+            k = j % self.n_streams
+            st, rz = self.streams[k], self.rz[k]
+            with torch.cuda.stream(st):
+                rz.prepare(cam, st)
+                rz.prune_score(score, bg, stream=st)
+        for st in self.streams:
+            cur.wait_stream(st)
+        return score
+
+
 def render_views_to_host(pipe: "FramePipeline", cams, host_out: list, bg=(0.0, 0.0, 0.0)) -> None:
     """End-to-end public call: render each camera and land its image in pinned host memory.
 

@@ -35,3 +35,26 @@ def test_pipeline_images_equal_single_stream(n_streams):
     render_views_to_host(pipe, cams, host, (0.1, 0.0, 0.2))
     for j in range(len(cams)):
         assert np.array_equal(host[j].numpy(), ref[j]), j
+
+
+def test_pipeline_score_views_equal_single_stream():
+    """a7 over several views with frames in flight = the single-stream accumulation (float64
+    atomics: equal up to summation order)."""
+    from paper_2412_00578_b200.raster import DeviceScene, FramePipeline, Rasterizer, camera_struct
+    scene = synth.orbit_scene(30000, 6)
+    cams = synth.orbit_cameras(7, 200, 136)
+    ds = DeviceScene.from_host(scene)
+    rz = Rasterizer(ds, 200, 136)
+    ref = torch.zeros(scene.n, dtype=torch.float64, device="cuda")
+    for c in cams:
+        rz.ensure_capacity(c)
+        rz.prepare(c)
+        rz.prune_score(ref, (0.2, 0.1, 0.0))
+    pipe = FramePipeline(ds, 200, 136, n_streams=3)
+    pipe.ensure_capacity(cams)
+    got = torch.zeros(scene.n, dtype=torch.float64, device="cuda")
+    pipe.score_views([camera_struct(c) for c in cams], got, (0.2, 0.1, 0.0))
+    torch.cuda.synchronize()
+    r, g = ref.cpu().numpy(), got.cpu().numpy()
+    assert (r > 0).sum() > 1000
+    assert np.allclose(g, r, rtol=1e-12, atol=1e-300)
