@@ -174,3 +174,29 @@ def test_schedule_prunes_inside_training():
         assert k == int(np.floor(ratio * n)) and n_after == n - k
         n = n_after
     assert tr.n == n and len(hist["events"]) == len(sched)
+
+
+def test_prune_keeps_optimizer_state_aligned():
+    """After a prune event the Adam state rows belong to the surviving Gaussians: raw = the
+    inverse activation of the (compacted) scene, and m / v are the compacted pre-prune rows."""
+    from paper_2412_00578_b200.raster import DeviceScene
+    from paper_2412_00578_b200.train import Trainer, render_targets
+    gt, cams = _small_orbit(n=6000, views=4, W=128, H=96)
+    targets = render_targets(DeviceScene.from_host(gt), cams)
+    tr = Trainer(DeviceScene.from_host(synth.perturb(gt, seed=3)), cams, targets)
+    tr.fit(20)
+    m_before = tr.m.mean_opac.cpu().numpy().copy()
+    score = tr.score()
+    from paper_2412_00578_b200.raster import prune_select
+    keep, k = prune_select(score, 0.5)
+    tr.prune_mask(keep, tr.n - k)
+    kept = np.nonzero(keep.cpu().numpy())[0]
+    assert tr.n == len(kept)
+    assert np.array_equal(tr.m.mean_opac.cpu().numpy(), m_before[kept])
+    mo, raw = tr.scene.mean_opac.cpu().numpy(), tr.raw.mean_opac.cpu().numpy()
+    assert np.array_equal(mo[:, :3], raw[:, :3])
+    assert np.allclose(mo[:, 3], 1.0 / (1.0 + np.exp(-raw[:, 3].astype(np.float64))), rtol=1e-6)
+    sc, rs = tr.scene.scale.cpu().numpy()[:, :3], tr.raw.scale.cpu().numpy()[:, :3]
+    assert np.allclose(sc, np.exp(rs.astype(np.float64)), rtol=1e-6)
+    tr.fit(5)   # training continues on the pruned scene
+    assert np.isfinite(tr.scene.mean_opac.cpu().numpy()).all()
