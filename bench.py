@@ -227,7 +227,7 @@ def run_ours(args):
         rz = Rasterizer(ds, W, H, mode=args.mode, capacity=max(1024, 8 * ds.n))
 
     # sizing + per-view statistics (untimed): pairs per frame, visible counts, render work
-    pairs, nvis, E_pix, E_blend, E_cta, E_kept, ncol = {}, {}, {}, {}, {}, {}, {}
+    pairs, nvis, E_pix, E_blend, E_cta, ncol = {}, {}, {}, {}, {}, {}
     for v in my_views:
         rz.ensure_capacity(cams[v])
     cap = rz.capacity
@@ -239,7 +239,7 @@ def run_ours(args):
         pairs[v], nvis[v] = t["pairs"], t["n_visible"]
         ncol[v] = int(((rz.records()[:, 8] == 1.0) & (rz.depth_keys() != -1)).sum().item())
         st = rz.render_stats()
-        E_pix[v], E_blend[v], E_cta[v], E_kept[v] = st["E_pix"], st["E_blend"], st["E_cta"], st["E_kept"]
+        E_pix[v], E_blend[v], E_cta[v] = st["E_pix"], st["E_blend"], st["E_cta"]
     # shrink capacity to the measured maximum (+2%) so the per-frame memset is tight
     rz._alloc(int(max(pairs.values()) * 1.02) + 4096)
 
@@ -544,7 +544,7 @@ def run_ours(args):
             "host_enqueue_ms_per_frame": host_ms,
             "stages": stage_info,
             "render_work": {"E_pix": mean(E_pix), "E_blend": mean(E_blend), "E_cta": mean(E_cta),
-                            "E_kept_after_warp_cull": mean(E_kept), "pixels": W * H},
+                            "pixels": W * H},
             "stages_timing": "single-stream pass of V frames after the timed region (every stage bracketed by events)",
             "roofline": roof,
             # ours per frame: k_preprocess, 4 x k_onesweep, k_escan_reduce, k_escan_apply, k_entries,

@@ -2,9 +2,10 @@
 // NEXT-2 render backward.
 //
 // One CTA per 16x16 tile, one thread per pixel ("parallelized across pixels").  The
-// tile's depth-ordered Gaussian ids are consumed in batches of 256: each thread gathers one
-// 48 B record into shared memory, then every pixel walks the batch.  A CTA stops as soon
-// as all of its pixels are saturated (__syncthreads_count).
+// tile's depth-ordered Gaussian ids are consumed in batches of kBatch = 128: one thread per
+// slot gathers the 48 B record into shared memory (computing the view-dependent colour on
+// first use, ss_color.cuh), then every still-active pixel walks the batch.  Before every batch
+// the active pixels are compacted onto the lowest threads; a CTA stops as soon as none is left.
 //
 // Arithmetic contract: the alpha-skip decision q <= t (alpha >= 1/255, Eq. 9)
 // uses the pinned chain u = fma(a, dx, (2b) dy); q = fma(dx, u, (c dy) dy) with explicit
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
 // the same per-pixel walk as k_render.  counters[0] += E_pix (evaluations each pixel makes
 // until it terminates, the method's work), [1] += E_blend (evaluations that blend),
 // [2] += E_cta (evaluations a CTA issues in lock-step until its last pixel terminates:
-// 256 x Gaussians staged), [3] += pixels, [4] += evaluations left after per-warp culling.
+// 256 x Gaussians staged), [3] += pixels; [4] is reserved (left 0).
 __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ ranges,
                                                       const uint32_t *__restrict__ vals,
                                                       const float4 *__restrict__ rec, int W, int H, int tiles_x,
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ 
     const uint2 range = ranges[tile];
     bool done = !inside;
     float T = 1.0f;
-    unsigned long long e_pix = 0, e_blend = 0, e_cta = 0, e_warp = 0;
+    unsigned long long e_pix = 0, e_blend = 0, e_cta = 0;
     if (threadIdx.x < 5) s_acc[threadIdx.x] = 0;
     for (uint32_t start = range.x; start < range.y; start += kBatch) {
         if (__syncthreads_count(done) == blockDim.x) break;
@@ -554,7 +555,6 @@ __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ 
         atomicAdd(counters + 1, s_acc[1]);
         atomicAdd(counters + 2, e_cta * blockDim.x);
         atomicAdd(counters + 3, (unsigned long long)n_inside);
-        atomicAdd(counters + 4, e_warp);
     }
 }
 
