@@ -23,7 +23,7 @@ import torch
 
 from . import dist
 from ._abi import SsAdamConfig, check, lib
-from .raster import DeviceScene, Rasterizer, _stream_handle, camera_struct, compact, prune_select
+from .raster import DeviceScene, FramePipeline, Rasterizer, _stream_handle, camera_struct, compact, prune_select
 
 
 @dataclass
@@ -145,15 +145,17 @@ class Trainer:
         return v
 
     # ------------------------------------------------------------------ pruning
-    def score(self) -> torch.Tensor:
-        """Ũ over every training view (this rank's shard, then the float64 all_reduce)."""
-        def score_view(v, s):
-            self.rz.prepare(self.cstructs[v])
-            if self.rz.totals()["overflow"]:
-                self.rz.ensure_capacity(self.cams[v])
-                self.rz.prepare(self.cstructs[v])
-            self.rz.prune_score(s, self.bg)
-        return dist.accumulate_scores(score_view, len(self.cams), self.n, self.dev)
+    def score(self, n_streams: int = 3) -> torch.Tensor:
+        """Ũ over every training view: this rank's shard of the views with several frames in
+        flight (FramePipeline.score_views), then the float64 all_reduce."""
+        rank, world, _ = dist.world()
+        mine = dist.views_for_rank(len(self.cams), rank, world)
+        score = torch.zeros(self.n, dtype=torch.float64, device=self.dev)
+        if mine:
+            pipe = FramePipeline(self.scene, self.W, self.H, mode=self.mode, n_streams=n_streams)
+            pipe.ensure_capacity([self.cams[v] for v in mine], headroom=1.05)
+            pipe.score_views([self.cstructs[v] for v in mine], score, self.bg)
+        return dist.allreduce_scores(score)
 
     def prune(self, ratio: float, score: torch.Tensor | None = None) -> int:
         """Remove ⌊ratio·N⌋ lowest-Ũ Gaussians with their Adam state; returns the removed count."""
