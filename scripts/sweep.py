@@ -84,7 +84,7 @@ def main():
         print(json.dumps({"workload": name, "speedup_vs_3sigma": {m: res[m]["fps"] / base for m in res},
                           "pairs_ratio_3sigma_over": {m: res["3sigma"]["pairs_per_frame"] / res[m]["pairs_per_frame"]
                                                       for m in res}}), flush=True)
-        if name == "mnr360-3m":  # pruned-model regime: score all views, drop 90%, AccuTile
+        if True:  # pruned-model regime (BASELINE config 5): score all views, drop 90%, AccuTile
             rz = Rasterizer(ds, cams[0].width, cams[0].height, mode="accutile", capacity=4 * scene.n)
             score = torch.zeros(scene.n, dtype=torch.float64, device="cuda")
             for cam in cams:
