@@ -269,7 +269,7 @@ class FramePipeline:
     (measured on B200, MNR360-3M: 1 stream 1263 frames/s, 2 -> 1470, 3 -> 1538, 4 -> 1544).
     Within a stream the frame's kernels keep their programmatic dependent launches."""
 
-    def __init__(self, scene: DeviceScene, width: int, height: int, mode: str = "accutile", n_streams: int = 3,
+    def __init__(self, scene: DeviceScene, width: int, height: int, mode: str = "accutile", n_streams: int = 4,
                  capacity: int | None = None):
         self.n_streams = int(n_streams)
         self.width, self.height = int(width), int(height)
