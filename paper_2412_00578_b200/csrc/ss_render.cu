@@ -272,8 +272,10 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
                         const float4 cl = s.col[k];
                         const float alpha = alpha_of(q, cl.w);
                         const float om = 1.0f - alpha;
-                        T = T / om;
-                        const float bgs = Tfin / om;
+                        float rom;  // T_i = T_{i+1} / (1 - alpha_i): one approximate reciprocal
+                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rom) : "f"(om));
+                        T = T * rom;
+                        const float bgs = Tfin * rom;
                         const float d0 = T * (cl.x - S0) - bgs * bg0;
                         const float d1 = T * (cl.y - S1) - bgs * bg1;
                         const float d2 = T * (cl.z - S2) - bgs * bg2;
