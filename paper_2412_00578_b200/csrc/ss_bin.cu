@@ -24,6 +24,8 @@
 #include "ss_tilegeom.cuh"
 
 namespace ss {
+
+constexpr int kEntriesCtasPerSm = 8;  // k_entries grid (grid-stride over the visible Gaussians)
 namespace {
 
 constexpr int kScanThreads = 256;
@@ -718,7 +720,7 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
     const uint32_t *E = ctr + 8;
     int sbits = 1;
     while ((1 << sbits) < L.n_super) ++sbits;
-    launch_pdl(k_entries, sms * 8, 256, 0, st, at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, P.overflow),
+    launch_pdl(k_entries, sms * kEntriesCtasPerSm, 256, 0, st, at<const uint32_t>(ws, P.n_visible), at<const uint32_t>(ws, P.overflow),
                                        at<const uint32_t>(ws, L.eoff), at<const uint32_t>(ws, P.order),
                                        at<const uint4>(ws, P.erec), at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y,
                                        L.stx, at<uint2>(ws, L.stg), ctr + 12, at<uint32_t>(ws, L.big_queue));

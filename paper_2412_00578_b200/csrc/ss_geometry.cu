@@ -292,7 +292,7 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
     if (sc.n == 0) return cudaSuccess;
     const int sms = sm_count();
     const int blocks_needed = (sc.n + kPreThreads - 1) / kPreThreads;
-    const int resident = sms * kPreBlocks * 4;  // four rounds of resident CTAs
+    const int resident = sms * kPreBlocks;  // one round of resident CTAs (persistent; measured: 1 round 1624 fps, 2: 1615, 4: 1591, 8: 1576)
     const int grid = blocks_needed < resident ? blocks_needed : resident;
 #define SS_PRE_ARGS                                                                                       \
     sc.n, reinterpret_cast<const float4 *>(sc.mean_opac), reinterpret_cast<const float4 *>(sc.scale),         \
