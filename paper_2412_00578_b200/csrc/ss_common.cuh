@@ -25,8 +25,8 @@ struct CamArgs {
 
 // Depth-sort geometry (onesweep LSD radix sort).
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 8;
-constexpr int kSortTile = kSortThreads * kSortItems;   // 4096 keys per block tile
+constexpr int kSortItems = 12;
+constexpr int kSortTile = kSortThreads * kSortItems;   // 3072 keys per block tile
 constexpr int kInlineEnt = 6;                          // super-tile entries stored in the emission record
 constexpr int kLaneRows = 6;                           // AccuTile lines a preprocess lane sweeps alone
 constexpr int kDepthPasses = 4;                        // 32-bit depth keys, 8-bit digits

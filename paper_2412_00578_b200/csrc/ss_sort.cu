@@ -21,7 +21,7 @@ __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
 
 // One onesweep pass.  Block tickets (atomicAdd) give every CTA tile an id in launch order,
 // so a CTA only waits on ids already owned by running CTAs (forward progress).  Per tile:
-//  1. load 16 keys / thread, warp-striped (warp w owns [w*512, (w+1)*512) of the tile);
+//  1. load kSortItems keys / thread, warp-striped (warp w owns 32 kSortItems consecutive keys);
 //  2. warp-level stable ranking by 8 ballots per item (match on the digit), per-warp digit
 //     histograms in shared memory;
 //  3. digit totals -> look-back publication (aggregate, then inclusive prefix);
