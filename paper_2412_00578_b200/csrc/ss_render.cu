@@ -214,10 +214,12 @@ __global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ r
             float T = st.T[pp];
             uint32_t last = st.last[pp];
             bool done = false;
-            const int cnt = min((uint32_t)kBatch, range.y - start);
+            // groups of 4 over the padded batch (padding slots never contribute), as in k_render
+            const int cnt = ((int)min((uint32_t)kBatch, range.y - start) + 3) & ~3;
             const uint32_t base = start - range.x + 1;
-#pragma unroll 4
-            for (int k = 0; k < cnt; ++k) {  // branch-free, as in k_render
+            for (int k4 = 0; k4 < cnt && !done; k4 += 4)
+#pragma unroll
+            for (int k = k4; k < k4 + 4; ++k) {  // branch-free, as in k_render
                 const float4 bx = s.box[k];
                 const float4 cn = s.con[k];
                 const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
