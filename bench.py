@@ -482,13 +482,18 @@ def run_ours(args):
         tr.events = None
         ms_t = dist.max_over_ranks(a.elapsed_time(b))
         adam_ms = sum(x.elapsed_time(y) for x, y in aev) / n_it
-        # Adam: per Gaussian reads grad, raw, m, v and writes raw, m, v, the activated array:
-        # 8 passes over the scene's 240 B (mean_opac, scale, rot, 12 SH float4)
-        adam_bytes = 8 * 16 * (3 + {0: 1, 1: 3, 2: 7, 3: 12}[scene.sh_degree]) * ds.n
-        train_info = {"iters_per_s": world * n_it / (ms_t / 1e3), "iters": world * n_it,
+        # Adam (flagged): per Gaussian reads raw, m, v and writes raw, m, v, the activated array (7
+        # passes over the scene's 240 B: mean_opac, scale, rot, 12 SH float4), plus the gradient of
+        # the flagged (blended) Gaussians and one flag byte per Gaussian
+        slot_bytes = 16 * (3 + {0: 1, 1: 3, 2: 7, 3: 12}[scene.sh_degree])
+        n_flag = int(tr.flags.sum().item())
+        adam_bytes = 7 * slot_bytes * ds.n + slot_bytes * n_flag + ds.n
+        train_info = {"iters_per_s": world * n_it / (ms_t / 1e3), "iters": world * n_it, "flagged": n_flag,
                       "note": "one view per iteration (replica per rank): a1-a6 with T/n_contrib, ss_l1_loss_grad, "
-                              "ss_render_backward, ss_preprocess_backward, ss_adam_step over all N Gaussians "
-                              "(dense Adam, as 3D-GS); targets uniform random; capacity sized up front",
+                              "ss_render_backward, ss_preprocess_backward_assign (gradients written for the "
+                              "blended Gaussians, flagged), ss_adam_step_flagged over all N Gaussians (dense "
+                              "Adam, as 3D-GS; unflagged gradients are zero); targets uniform random; capacity "
+                              "sized up front",
                       "adam": {"ms": adam_ms, "bound": "hbm", "bytes": adam_bytes,
                                "achieved": adam_bytes / (adam_ms / 1e3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
                                "frac": adam_bytes / (adam_ms / 1e3) / 1e9 / hbm_peak}}

@@ -250,6 +250,14 @@ typedef struct {
 SS_API ss_status ss_preprocess_backward(const ss_scene *scene /*host*/, const ss_camera *cam /*host*/,
                                         const float *grad2d, const ss_scene_grad *grad /*host*/, void *stream);
 
+/* Variant for a training step (one view per step): the gradients of the Gaussians with a non-zero
+ * grad2d row are WRITTEN (=), not accumulated, and flags[i] (device uint8 [n], caller-zeroed) is
+ * set to 1 for each of them; the other Gaussians' gradient entries are left untouched (stale) and
+ * must be read as zero -- ss_adam_step_flagged does -- so the gradient arrays need no zeroing. */
+SS_API ss_status ss_preprocess_backward_assign(const ss_scene *scene /*host*/, const ss_camera *cam /*host*/,
+                                               const float *grad2d, const ss_scene_grad *grad /*host*/,
+                                               uint8_t *flags, void *stream);
+
 /* ---- NEXT-3: the optimisation step around the backward (Eq. 2, "optimized via
  * stochastic gradient descent on image reconstruction losses"; L1 term only, the D-SSIM term
  * is omitted -- SPEC S:421).
@@ -277,6 +285,14 @@ SS_API ss_status ss_adam_init(const ss_scene *scene /*host*/, const ss_scene_gra
 SS_API ss_status ss_adam_step(const ss_scene_grad *grad /*host*/, const ss_scene_grad *raw /*host*/,
                               const ss_scene_grad *m /*host*/, const ss_scene_grad *v /*host*/,
                               const ss_scene_grad *scene /*host*/, const ss_adam_config *cfg /*host*/, void *stream);
+
+/* ss_adam_step with gradient flags (ss_preprocess_backward_assign): a Gaussian whose flag is 0 has
+ * a zero gradient and its grad entries are not read; the update is otherwise ss_adam_step's
+ * (dense Adam: its moments still decay and its raw parameters still move by m / sqrt(v)). */
+SS_API ss_status ss_adam_step_flagged(const ss_scene_grad *grad /*host*/, const ss_scene_grad *raw /*host*/,
+                                      const ss_scene_grad *m /*host*/, const ss_scene_grad *v /*host*/,
+                                      const ss_scene_grad *scene /*host*/, const ss_adam_config *cfg /*host*/,
+                                      const uint8_t *flags, void *stream);
 
 /* Convenience: ss_preprocess + ss_bin + ss_sort + ss_render in one call. */
 SS_API ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,

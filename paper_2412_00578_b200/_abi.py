@@ -15,7 +15,8 @@ MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}
 EXPORTS = ["ss_frame_workspace_size", "ss_frame_layout", "ss_preprocess", "ss_bin", "ss_sort", "ss_sorted_keys",
            "ss_render", "ss_render_stats", "ss_finalize_colours", "ss_prune_score", "ss_render_frame",
            "ss_prune_workspace_size", "ss_prune_count", "ss_prune_select", "ss_compact_scene",
-           "ss_render_backward", "ss_preprocess_backward", "ss_l1_loss_grad", "ss_adam_init", "ss_adam_step", "ss_status_string", "ss_last_cuda_error", "ss_version"]
+           "ss_render_backward", "ss_preprocess_backward", "ss_l1_loss_grad", "ss_adam_init", "ss_adam_step",
+           "ss_preprocess_backward_assign", "ss_adam_step_flagged", "ss_status_string", "ss_last_cuda_error", "ss_version"]
 
 
 class SsScene(C.Structure):
@@ -81,6 +82,9 @@ def lib() -> C.CDLL:
             "ss_l1_loss_grad": (st, [C.c_int64, vp, vp, vp, vp, vp]),
             "ss_adam_init": (st, [P(SsScene), P(SsScene), P(SsScene), P(SsScene), vp]),
             "ss_adam_step": (st, [P(SsScene), P(SsScene), P(SsScene), P(SsScene), P(SsScene), P(SsAdamConfig), vp]),
+            "ss_preprocess_backward_assign": (st, [P(SsScene), P(SsCamera), vp, P(SsScene), vp, vp]),
+            "ss_adam_step_flagged": (st, [P(SsScene), P(SsScene), P(SsScene), P(SsScene), P(SsScene),
+                                          P(SsAdamConfig), vp, vp]),
             "ss_status_string": (C.c_char_p, [st]),
             "ss_last_cuda_error": (C.c_char_p, []),
             "ss_version": (C.c_char_p, []),

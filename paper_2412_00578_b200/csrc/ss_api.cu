@@ -231,8 +231,8 @@ ss_status ss_render_backward(const ss_frame *frame, const float *bg, const float
                                               T_final, n_contrib, grad2d, static_cast<cudaStream_t>(stream)));
 }
 
-ss_status ss_preprocess_backward(const ss_scene *scene, const ss_camera *cam, const float *grad2d,
-                                 const ss_scene_grad *grad, void *stream) {
+static ss_status preprocess_backward(const ss_scene *scene, const ss_camera *cam, const float *grad2d,
+                                     const ss_scene_grad *grad, uint8_t *flags, void *stream) {
     if (!scene || !cam || !grad || scene->n < 0 || scene->sh_degree < 0 || scene->sh_degree > 3) return SS_ERR_INVALID_ARG;
     if (grad->n != scene->n || grad->sh_degree != scene->sh_degree) return SS_ERR_INVALID_ARG;
     if (scene->n >= (1 << 30)) return SS_ERR_UNSUPPORTED;
@@ -242,8 +242,19 @@ ss_status ss_preprocess_backward(const ss_scene *scene, const ss_camera *cam, co
         return SS_ERR_INVALID_ARG;
     Layout L;
     if (!compute_layout(scene->n, 0, cam->width, cam->height, &L)) return SS_ERR_INVALID_ARG;
-    return cuda_status(launch_preprocess_backward(*scene, cam_args(*cam, L), grad2d, *grad,
+    return cuda_status(launch_preprocess_backward(*scene, cam_args(*cam, L), grad2d, *grad, flags,
                                                   static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_preprocess_backward(const ss_scene *scene, const ss_camera *cam, const float *grad2d,
+                                 const ss_scene_grad *grad, void *stream) {
+    return preprocess_backward(scene, cam, grad2d, grad, nullptr, stream);
+}
+
+ss_status ss_preprocess_backward_assign(const ss_scene *scene, const ss_camera *cam, const float *grad2d,
+                                        const ss_scene_grad *grad, uint8_t *flags, void *stream) {
+    if (!flags && scene && scene->n > 0) return SS_ERR_INVALID_ARG;
+    return preprocess_backward(scene, cam, grad2d, grad, flags, stream);
 }
 
 static bool grad_ok(const ss_scene_grad *g, int32_t n, int32_t deg) {
@@ -267,8 +278,9 @@ ss_status ss_adam_init(const ss_scene *scene, const ss_scene_grad *raw, const ss
     return cuda_status(launch_adam_init(*scene, *raw, *m, *v, static_cast<cudaStream_t>(stream)));
 }
 
-ss_status ss_adam_step(const ss_scene_grad *grad, const ss_scene_grad *raw, const ss_scene_grad *m,
-                       const ss_scene_grad *v, const ss_scene_grad *scene, const ss_adam_config *cfg, void *stream) {
+static ss_status adam_step(const ss_scene_grad *grad, const ss_scene_grad *raw, const ss_scene_grad *m,
+                           const ss_scene_grad *v, const ss_scene_grad *scene, const ss_adam_config *cfg,
+                           const uint8_t *flags, void *stream) {
     if (!grad || !cfg || grad->n < 0 || grad->sh_degree < 0 || grad->sh_degree > 3) return SS_ERR_INVALID_ARG;
     const int32_t n = grad->n, d = grad->sh_degree;
     if (!grad_ok(grad, n, d) || !grad_ok(raw, n, d) || !grad_ok(m, n, d) || !grad_ok(v, n, d) || !grad_ok(scene, n, d))
@@ -276,7 +288,21 @@ ss_status ss_adam_step(const ss_scene_grad *grad, const ss_scene_grad *raw, cons
     if (cfg->step < 1 || !(cfg->beta1 >= 0.0f && cfg->beta1 < 1.0f) || !(cfg->beta2 >= 0.0f && cfg->beta2 < 1.0f) ||
         !(cfg->eps >= 0.0f))
         return SS_ERR_INVALID_ARG;
-    return cuda_status(launch_adam_step(*grad, *raw, *m, *v, *scene, *cfg, static_cast<cudaStream_t>(stream)));
+    const int64_t blocks_sh = ((int64_t)(d + 1) * (d + 1) * 3 + 3) / 4;
+    if ((int64_t)n * blocks_sh >= (int64_t)1 << 31) return SS_ERR_UNSUPPORTED;  // 32-bit slot indexing
+    return cuda_status(launch_adam_step(*grad, *raw, *m, *v, *scene, *cfg, flags, static_cast<cudaStream_t>(stream)));
+}
+
+ss_status ss_adam_step(const ss_scene_grad *grad, const ss_scene_grad *raw, const ss_scene_grad *m,
+                       const ss_scene_grad *v, const ss_scene_grad *scene, const ss_adam_config *cfg, void *stream) {
+    return adam_step(grad, raw, m, v, scene, cfg, nullptr, stream);
+}
+
+ss_status ss_adam_step_flagged(const ss_scene_grad *grad, const ss_scene_grad *raw, const ss_scene_grad *m,
+                               const ss_scene_grad *v, const ss_scene_grad *scene, const ss_adam_config *cfg,
+                               const uint8_t *flags, void *stream) {
+    if (!flags && grad && grad->n > 0) return SS_ERR_INVALID_ARG;
+    return adam_step(grad, raw, m, v, scene, cfg, flags, stream);
 }
 
 ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,

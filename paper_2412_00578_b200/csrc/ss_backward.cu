@@ -52,9 +52,10 @@ __device__ __forceinline__ void sh_basis_grad(float x, float y, float z, float *
     Y[15] = E0 * x * (xx - 3.f * yy);         dX[15] = E0 * 3.f * (xx - yy);  dY[15] = -6.f * E0 * x * y;
 }
 
-// The chain rule for one Gaussian i with a non-zero 2D gradient (g0, g1, gbl).
-template <int DEG>
-__device__ __forceinline__ void backward_one(int i, float4 g0, float4 g1, float gbl,
+// The chain rule for one Gaussian i with a non-zero 2D gradient (g0, g1, gbl).  ASSIGN: the
+// gradients are written (=) instead of accumulated (+=).  Returns whether they were written.
+template <int DEG, bool ASSIGN>
+__device__ __forceinline__ bool backward_one(int i, float4 g0, float4 g1, float gbl,
                                              const float4 *__restrict__ mean_opac, const float4 *__restrict__ scale,
                                              const float4 *__restrict__ rot, const float4 *__restrict__ sh,
                                              const CamArgs &cam, float4 *__restrict__ d_mean_opac,
@@ -69,7 +70,7 @@ __device__ __forceinline__ void backward_one(int i, float4 g0, float4 g1, float 
     const float px = V[0] * mo.x + V[1] * mo.y + V[2] * mo.z + V[3];
     const float py = V[4] * mo.x + V[5] * mo.y + V[6] * mo.z + V[7];
     const float pz = V[8] * mo.x + V[9] * mo.y + V[10] * mo.z + V[11];
-    if (!(pz >= cam.z_near)) return;
+    if (!(pz >= cam.z_near)) return false;
     const float iz = 1.0f / pz, iz2 = iz * iz;
     const float tx = px * iz, ty = py * iz;
     float txc = tx, tyc = ty;
@@ -115,8 +116,9 @@ __device__ __forceinline__ void backward_one(int i, float4 g0, float4 g1, float 
     const float cxy = TS[0][0] * T[1][0] + TS[0][1] * T[1][1] + TS[0][2] * T[1][2];
     const float cyy = TS[1][0] * T[1][0] + TS[1][1] * T[1][1] + TS[1][2] * T[1][2] + 0.3f;
     const float det = cxx * cyy - cxy * cxy;
-    if (!(det > 0.0f)) return;
-    float4 dmo = d_mean_opac[i];
+    if (!(det > 0.0f)) return false;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 dmo = ASSIGN ? z4 : d_mean_opac[i];
     float dmu[3] = {0.f, 0.f, 0.f};
     // ---- colour (R13): clamped channels pass nothing
     {
@@ -132,7 +134,7 @@ __device__ __forceinline__ void backward_one(int i, float4 g0, float4 g1, float 
 #pragma unroll
         for (int p = 0; p < NP; ++p) {
             const float4 v = shi[p];
-            const float4 d = dshi[p];
+            const float4 d = ASSIGN ? z4 : dshi[p];
             h[4 * p + 0] = v.x; h[4 * p + 1] = v.y; h[4 * p + 2] = v.z; h[4 * p + 3] = v.w;
             dh[4 * p + 0] = d.x; dh[4 * p + 1] = d.y; dh[4 * p + 2] = d.z; dh[4 * p + 3] = d.w;
         }
@@ -219,7 +221,7 @@ __device__ __forceinline__ void backward_one(int i, float4 g0, float4 g1, float 
             ds[k] += dM * R[r][k];
             dR[r][k] = dM * s3[k];
         }
-    float4 dsc = d_scale[i];
+    float4 dsc = ASSIGN ? z4 : d_scale[i];
     dsc.x += ds[0];
     dsc.y += ds[1];
     dsc.z += ds[2];
@@ -233,12 +235,13 @@ __device__ __forceinline__ void backward_one(int i, float4 g0, float4 g1, float 
     dq[3] = 2.f * (-2.f * z * dR[0][0] - w * dR[0][1] + x * dR[0][2] + w * dR[1][0] - 2.f * z * dR[1][1] +
                    y * dR[1][2] + x * dR[2][0] + y * dR[2][1]);
     const float qd = w * dq[0] + x * dq[1] + y * dq[2] + z * dq[3];
-    float4 drt = d_rot[i];
+    float4 drt = ASSIGN ? z4 : d_rot[i];
     drt.x += (dq[0] - w * qd) * qi;
     drt.y += (dq[1] - x * qd) * qi;
     drt.z += (dq[2] - y * qd) * qi;
     drt.w += (dq[3] - z * qd) * qi;
     d_rot[i] = drt;
+    return true;
 }
 
 constexpr int kBwdChunk = 4096;  // Gaussians scanned per CTA and round
@@ -248,7 +251,7 @@ constexpr int kBwdChunk = 4096;  // Gaussians scanned per CTA and round
 // grad2d rows (coalesced, 48 B per Gaussian), compacts the non-zero ones into a shared-memory
 // list (warp ballots, one shared atomic per warp), then runs the chain rule with one thread per
 // listed Gaussian -- full warps instead of one busy lane per warp.
-template <int DEG>
+template <int DEG, bool ASSIGN>
 __global__ void __launch_bounds__(256, 2) k_preprocess_backward(int n, const float4 *__restrict__ mean_opac,
                                                              const float4 *__restrict__ scale,
                                                              const float4 *__restrict__ rot,
@@ -256,7 +259,8 @@ __global__ void __launch_bounds__(256, 2) k_preprocess_backward(int n, const flo
                                                              const float4 *__restrict__ grad2d,
                                                              float4 *__restrict__ d_mean_opac,
                                                              float4 *__restrict__ d_scale, float4 *__restrict__ d_rot,
-                                                             float4 *__restrict__ d_sh) {
+                                                             float4 *__restrict__ d_sh,
+                                                             uint8_t *__restrict__ flags) {
     pdl_enter();
     __shared__ uint32_t s_list[kBwdChunk];
     __shared__ uint32_t s_cnt;
@@ -284,8 +288,10 @@ __global__ void __launch_bounds__(256, 2) k_preprocess_backward(int n, const flo
         const uint32_t cnt = s_cnt;
         for (uint32_t j = threadIdx.x; j < cnt; j += blockDim.x) {
             const int i = (int)s_list[j];
-            backward_one<DEG>(i, grad2d[3 * (size_t)i + 0], grad2d[3 * (size_t)i + 1], grad2d[3 * (size_t)i + 2].x,
-                              mean_opac, scale, rot, sh, cam, d_mean_opac, d_scale, d_rot, d_sh);
+            const bool w = backward_one<DEG, ASSIGN>(i, grad2d[3 * (size_t)i + 0], grad2d[3 * (size_t)i + 1],
+                                                     grad2d[3 * (size_t)i + 2].x, mean_opac, scale, rot, sh, cam,
+                                                     d_mean_opac, d_scale, d_rot, d_sh);
+            if (flags && w) flags[i] = 1;
         }
         __syncthreads();
     }
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(256, 2) k_preprocess_backward(int n, const flo
 }  // namespace
 
 cudaError_t launch_preprocess_backward(const ss_scene &sc, const CamArgs &cam, const float *grad2d,
-                                       const ss_scene_grad &out, cudaStream_t st) {
+                                       const ss_scene_grad &out, uint8_t *flags, cudaStream_t st) {
     if (sc.n == 0) return cudaSuccess;
     const int blocks = (int)std::min<int64_t>(((int64_t)sc.n + kBwdChunk - 1) / kBwdChunk, (int64_t)sm_count() * 4);
     auto mo = reinterpret_cast<const float4 *>(sc.mean_opac);
@@ -306,12 +312,18 @@ cudaError_t launch_preprocess_backward(const ss_scene &sc, const CamArgs &cam, c
     auto ds = reinterpret_cast<float4 *>(out.scale);
     auto dr = reinterpret_cast<float4 *>(out.rot);
     auto dsh = reinterpret_cast<float4 *>(out.sh);
+#define SS_BWD(D)                                                                                              \
+    (flags ? launch_pdl(k_preprocess_backward<D, true>, blocks, 256, 0, st, sc.n, mo, s4, r4, sh, cam, g, dmo, ds, \
+                        dr, dsh, flags)                                                                        \
+           : launch_pdl(k_preprocess_backward<D, false>, blocks, 256, 0, st, sc.n, mo, s4, r4, sh, cam, g, dmo,   \
+                        ds, dr, dsh, (uint8_t *)nullptr))
     switch (sc.sh_degree) {
-        case 0: launch_pdl(k_preprocess_backward<0>, blocks, 256, 0, st, sc.n, mo, s4, r4, sh, cam, g, dmo, ds, dr, dsh); break;
-        case 1: launch_pdl(k_preprocess_backward<1>, blocks, 256, 0, st, sc.n, mo, s4, r4, sh, cam, g, dmo, ds, dr, dsh); break;
-        case 2: launch_pdl(k_preprocess_backward<2>, blocks, 256, 0, st, sc.n, mo, s4, r4, sh, cam, g, dmo, ds, dr, dsh); break;
-        default: launch_pdl(k_preprocess_backward<3>, blocks, 256, 0, st, sc.n, mo, s4, r4, sh, cam, g, dmo, ds, dr, dsh); break;
+        case 0: SS_BWD(0); break;
+        case 1: SS_BWD(1); break;
+        case 2: SS_BWD(2); break;
+        default: SS_BWD(3); break;
     }
+#undef SS_BWD
     return cudaGetLastError();
 }
 

@@ -159,9 +159,9 @@ cudaError_t launch_adam_init(const ss_scene &sc, const ss_scene_grad &raw, const
                              const ss_scene_grad &v, cudaStream_t st);
 cudaError_t launch_adam_step(const ss_scene_grad &g, const ss_scene_grad &raw, const ss_scene_grad &m,
                              const ss_scene_grad &v, const ss_scene_grad &out, const ss_adam_config &c,
-                             cudaStream_t st);
+                             const uint8_t *flags, cudaStream_t st);
 cudaError_t launch_preprocess_backward(const ss_scene &sc, const CamArgs &cam, const float *grad2d,
-                                       const ss_scene_grad &out, cudaStream_t st);
+                                       const ss_scene_grad &out, uint8_t *flags, cudaStream_t st);
 
 size_t prune_workspace_bytes(int32_t n);
 cudaError_t launch_prune_select(const double *score, int32_t n, double ratio, uint8_t *keep, void *ws,

@@ -46,12 +46,12 @@ __global__ void __launch_bounds__(256) k_l1_loss_grad(int64_t count, const float
 }
 
 struct AdamArgs {
-    float lr_mean, lr_opacity, lr_scale, lr_rot, lr_sh_dc, lr_sh_rest, b1, b2, eps, c1, c2;  // c = 1 - b^t
+    float lr_mean, lr_opacity, lr_scale, lr_rot, lr_sh_dc, lr_sh_rest, b1, b2, eps, ic1, ic2;  // 1 / (1 - b^t)
 };
 
 // act: 0 identity, 1 exp, 2 sigmoid
 __device__ __forceinline__ float act_fwd(int act, float r) {
-    return act == 1 ? expf(r) : (act == 2 ? 1.0f / (1.0f + expf(-r)) : r);
+    return act == 1 ? __expf(r) : (act == 2 ? __fdividef(1.0f, 1.0f + __expf(-r)) : r);
 }
 
 __device__ __forceinline__ void adam1(float g_act, float &raw, float &m, float &v, float &out, int act, float lr,
@@ -60,7 +60,8 @@ __device__ __forceinline__ void adam1(float g_act, float &raw, float &m, float &
     const float g = g_act * (act == 1 ? a : (act == 2 ? a * (1.0f - a) : 1.0f));
     m = A.b1 * m + (1.0f - A.b1) * g;
     v = A.b2 * v + (1.0f - A.b2) * g * g;
-    raw -= lr * (m / A.c1) / (sqrtf(v / A.c2) + A.eps);
+    // bias corrections as products with host-side reciprocals, one fast division
+    raw -= __fdividef(lr * (m * A.ic1), sqrtf(v * A.ic2) + A.eps);
     out = act_fwd(act, raw);
 }
 
@@ -69,8 +70,10 @@ __device__ __forceinline__ void adam1(float g_act, float &raw, float &m, float &
 // read, raw, m, v and the activated array written (components a slot does not use -- scale.w,
 // SH padding -- keep raw == activated, as ss_adam_init set them).  mean_opac: xyz identity,
 // sigma sigmoid; scale: exp; rot: identity; SH: identity, coefficients 0..2 (DC) at lr_sh_dc.
+// flags (nullable): a Gaussian whose flag is 0 has zero gradient (its grad entries are not read).
 __global__ void __launch_bounds__(256) k_adam(int64_t n, int B, int nb3, ss_scene_grad g, ss_scene_grad raw,
-                                              ss_scene_grad m, ss_scene_grad v, ss_scene_grad out, AdamArgs A) {
+                                              ss_scene_grad m, ss_scene_grad v, ss_scene_grad out, AdamArgs A,
+                                              const uint8_t *__restrict__ flags) {
     pdl_enter();
     const int64_t total = n * (3 + B);
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
@@ -86,14 +89,17 @@ __global__ void __launch_bounds__(256) k_adam(int64_t n, int B, int nb3, ss_scen
         };
         float4 *const gp = pick(g), *const rp = pick(raw), *const mp = pick(m), *const vp = pick(v),
                      *const op = pick(out);
-        const float4 g4 = gp[e];
+        // the slot's Gaussian and SH coefficient (32-bit division: n * B < 2^31 is checked by the caller)
+        const uint32_t q = arr == 3 ? (uint32_t)e / (uint32_t)B : (uint32_t)e;
+        const int64_t gi = q;
+        const float4 g4 = (flags && !flags[gi]) ? make_float4(0.f, 0.f, 0.f, 0.f) : gp[e];
         float4 r4 = rp[e];
         float4 m4 = mp[e];
         float4 v4 = vp[e];
         float4 o4;
         const float *gr = (const float *)&g4;
         float *rr = (float *)&r4, *mr = (float *)&m4, *vr = (float *)&v4, *orr = (float *)&o4;
-        const int coef0 = arr == 3 ? (int)(e % B) * 4 : 0;
+        const int coef0 = arr == 3 ? (int)((uint32_t)e - q * (uint32_t)B) * 4 : 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             int act = 0, used = 1;
@@ -158,7 +164,7 @@ cudaError_t launch_adam_init(const ss_scene &sc, const ss_scene_grad &raw, const
 
 cudaError_t launch_adam_step(const ss_scene_grad &g, const ss_scene_grad &raw, const ss_scene_grad &m,
                              const ss_scene_grad &v, const ss_scene_grad &out, const ss_adam_config &c,
-                             cudaStream_t st) {
+                             const uint8_t *flags, cudaStream_t st) {
     if (g.n == 0) return cudaSuccess;
     AdamArgs A;
     A.lr_mean = c.lr_mean;
@@ -170,13 +176,13 @@ cudaError_t launch_adam_step(const ss_scene_grad &g, const ss_scene_grad &raw, c
     A.b1 = c.beta1;
     A.b2 = c.beta2;
     A.eps = c.eps;
-    A.c1 = (float)(1.0 - std::pow((double)c.beta1, (double)c.step));
-    A.c2 = (float)(1.0 - std::pow((double)c.beta2, (double)c.step));
+    A.ic1 = (float)(1.0 / (1.0 - std::pow((double)c.beta1, (double)c.step)));
+    A.ic2 = (float)(1.0 / (1.0 - std::pow((double)c.beta2, (double)c.step)));
     const int nb3 = (g.sh_degree + 1) * (g.sh_degree + 1) * 3;
     const int B = sh_blocks(g.sh_degree);
     const int64_t total = (int64_t)g.n * (3 + B);
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)sm_count() * 16);
-    launch_pdl(k_adam, blocks, 256, 0, st, (int64_t)g.n, B, nb3, g, raw, m, v, out, A);
+    launch_pdl(k_adam, blocks, 256, 0, st, (int64_t)g.n, B, nb3, g, raw, m, v, out, A, flags);
     return cudaGetLastError();
 }
 

@@ -96,6 +96,7 @@ class Trainer:
             self.rz.ensure_capacity(c, headroom=1.5)
         self.grads = scene.zeros_like()
         self.grad2d = torch.zeros((scene.n, 12), dtype=torch.float32, device=self.dev)
+        self.flags = torch.zeros(max(scene.n, 1), dtype=torch.uint8, device=self.dev)
         if init_state:
             self.raw, self.m, self.v = scene.zeros_like(), scene.zeros_like(), scene.zeros_like()
             s = scene.struct()
@@ -123,17 +124,22 @@ class Trainer:
                                     C.c_void_p(_stream_handle(None))), "ss_l1_loss_grad")
         self.grad2d.zero_()
         self.rz.render_backward(self.dimg, T, nc, grad2d=self.grad2d, bg=self.bg)
-        for t in (self.grads.mean_opac, self.grads.scale, self.grads.rot, self.grads.sh):
-            t.zero_()
-        self.rz.preprocess_backward(cam, self.grad2d, self.grads)
+        # the gradients of this view's blended Gaussians are written (not accumulated) and
+        # flagged; the others count as zero in Adam, so the gradient arrays are never zeroed
+        self.flags.zero_()
+        check(lib().ss_preprocess_backward_assign(C.byref(self.rz._scene_struct), C.byref(cam),
+                                                  C.c_void_p(self.grad2d.data_ptr()), C.byref(self.grads.struct()),
+                                                  C.c_void_p(self.flags.data_ptr()),
+                                                  C.c_void_p(_stream_handle(None))), "ss_preprocess_backward_assign")
         if self.events is not None:
             self.events[0].record()
         cfg = self.adam.struct(self.it)
         sc = self.scene
         out = DeviceScene(sc.mean_opac, sc.scale, sc.rot, sc.sh, sc.sh_degree)
-        check(lib().ss_adam_step(C.byref(self.grads.struct()), C.byref(self.raw.struct()), C.byref(self.m.struct()),
-                                 C.byref(self.v.struct()), C.byref(out.struct()), C.byref(cfg),
-                                 C.c_void_p(_stream_handle(None))), "ss_adam_step")
+        check(lib().ss_adam_step_flagged(C.byref(self.grads.struct()), C.byref(self.raw.struct()),
+                                         C.byref(self.m.struct()), C.byref(self.v.struct()), C.byref(out.struct()),
+                                         C.byref(cfg), C.c_void_p(self.flags.data_ptr()),
+                                         C.c_void_p(_stream_handle(None))), "ss_adam_step_flagged")
         if self.events is not None:
             self.events[1].record()
         self.n_loss_values = img.numel()

@@ -200,3 +200,62 @@ def test_prune_keeps_optimizer_state_aligned():
     assert np.allclose(sc, np.exp(rs.astype(np.float64)), rtol=1e-6)
     tr.fit(5)   # training continues on the pruned scene
     assert np.isfinite(tr.scene.mean_opac.cpu().numpy()).all()
+
+
+def test_assign_backward_and_flagged_adam_equal_the_dense_path():
+    """ss_preprocess_backward_assign writes exactly what ss_preprocess_backward accumulates into
+    zeroed arrays, flags exactly the Gaussians with a non-zero grad2d row and leaves the others'
+    entries untouched; ss_adam_step_flagged then equals ss_adam_step on the zero-filled gradients."""
+    import ctypes as C
+    from paper_2412_00578_b200._abi import check, lib
+    from paper_2412_00578_b200.raster import DeviceScene, Rasterizer, camera_struct
+    from paper_2412_00578_b200.train import AdamConfig
+    scene, cams = _small_orbit(n=8000, views=2, W=128, H=96)
+    ds = DeviceScene.from_host(scene)
+    rz = Rasterizer(ds, 128, 96)
+    rz.ensure_capacity(cams[0])
+    img, T, nc = rz.render_frame(cams[0], want_T=True, want_ncontrib=True)
+    dimg = torch.empty_like(img).uniform_(-1, 1)
+    g2d = rz.render_backward(dimg, T, nc)
+    dense = rz.preprocess_backward(cams[0], g2d)                      # += into zeros
+    stale = ds.zeros_like()
+    for t in (stale.mean_opac, stale.scale, stale.rot, stale.sh):
+        t.fill_(123.0)
+    flags = torch.zeros(scene.n, dtype=torch.uint8, device="cuda")
+    check(lib().ss_preprocess_backward_assign(C.byref(ds.struct()), C.byref(camera_struct(cams[0])),
+                                              C.c_void_p(g2d.data_ptr()), C.byref(stale.struct()),
+                                              C.c_void_p(flags.data_ptr()), None), "assign")
+    torch.cuda.synchronize()
+    f = flags.cpu().numpy().astype(bool)
+    assert np.array_equal(f, (g2d.cpu().numpy()[:, :9] != 0).any(1))
+    assert f.sum() > 100
+    for a, b in ((stale.mean_opac, dense.mean_opac), (stale.scale, dense.scale), (stale.rot, dense.rot),
+                 (stale.sh, dense.sh)):
+        an, bn = a.cpu().numpy(), b.cpu().numpy()
+        # same chain rule; the two template instantiations may contract the SH-basis polynomials
+        # into FMAs differently (a few float32 ulps)
+        assert np.allclose(an[f], bn[f], rtol=1e-6, atol=1e-12)
+        assert np.all(an[~f] == 123.0)
+    # flagged Adam on gradients whose unflagged rows are stale == dense Adam on zero-filled rows
+    fl = torch.from_numpy(f).cuda()
+    for t_stale, t_dense in ((stale.mean_opac, dense.mean_opac), (stale.scale, dense.scale), (stale.rot, dense.rot),
+                             (stale.sh, dense.sh)):
+        t_stale[fl] = t_dense[fl]
+    cfg = AdamConfig(extent=4.0).struct(1)
+    outs = []
+    for flagged in (False, True):
+        sc = DeviceScene(ds.mean_opac.clone(), ds.scale.clone(), ds.rot.clone(), ds.sh.clone(), ds.sh_degree)
+        raw, m, v = sc.zeros_like(), sc.zeros_like(), sc.zeros_like()
+        check(lib().ss_adam_init(C.byref(sc.struct()), C.byref(raw.struct()), C.byref(m.struct()), C.byref(v.struct()),
+                                 None), "init")
+        if flagged:
+            check(lib().ss_adam_step_flagged(C.byref(stale.struct()), C.byref(raw.struct()), C.byref(m.struct()),
+                                             C.byref(v.struct()), C.byref(sc.struct()), C.byref(cfg),
+                                             C.c_void_p(flags.data_ptr()), None), "flagged")
+        else:
+            check(lib().ss_adam_step(C.byref(dense.struct()), C.byref(raw.struct()), C.byref(m.struct()),
+                                     C.byref(v.struct()), C.byref(sc.struct()), C.byref(cfg), None), "dense")
+        torch.cuda.synchronize()
+        outs.append([t.cpu().numpy() for t in (sc.mean_opac, sc.scale, sc.rot, sc.sh, m.sh, v.mean_opac)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
