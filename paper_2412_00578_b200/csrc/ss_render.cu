@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256, 6) k_render(const uint2 *__restrict__ ran
 // Both walks compact the active pixels per batch like k_render.  Per batch, per-Gaussian
 // sums are reduced warp -> CTA in shared memory and added to the float64 score with one
 // atomic per (tile, Gaussian).
-__global__ void __launch_bounds__(256) k_prune_score(const uint2 *__restrict__ ranges,
+__global__ void __launch_bounds__(256, 6) k_prune_score(const uint2 *__restrict__ ranges,
                                                      const uint32_t *__restrict__ vals,
                                                      const float4 *__restrict__ rec, int W, int H, int tiles_x,
                                                      float bg0, float bg1, float bg2, double *__restrict__ score,
