@@ -10,6 +10,11 @@
  *   ss_render      per-tile front-to-back blending     Sec. 3.2.3, Eqs. 5-7
  *   ss_prune_score efficient pruning score, +=         Sec. 4.2.1, Eqs. 20-21
  *
+ * Beyond the forward path: the prune step (ss_prune_select,
+ * ss_compact_scene; Sec. 4.2), the backward (ss_render_backward, ss_preprocess_backward[_assign];
+ * P:404) and the optimisation step of pruning-in-the-loop training (ss_l1_loss_grad,
+ * ss_adam_init, ss_adam_step[_flagged]; Eq. 2).
+ *
  * The tile test of ss_preprocess / ss_bin is selected by ss_bin_mode: the 3D-GS 3-sigma
  * square (Eq. 8), SnugBox (Sec. 4.1.1, Eqs. 15-16) or AccuTile
  * (Sec. 4.1.2, Algorithm 1).
