@@ -296,6 +296,24 @@ class FramePipeline:
         cur = torch.cuda.current_stream()
         for st in self.streams:
             st.wait_stream(cur)
+        if pre_events is None and on_frame is None:
+            # the plain path: one C-ABI call per frame (ss_render_frame = a1-a6), no per-frame
+            # Python stream contexts -- the host enqueues a frame in a fraction of its GPU time
+            bgv = (C.c_float * 3)(*[float(v) for v in bg])
+            mode = MODES[self.rz[0].mode]
+            handles = [C.c_void_p(int(st.cuda_stream)) for st in self.streams]
+            fn = lib().ss_render_frame
+            for j, cam in enumerate(cams):
+                k = j % self.n_streams
+                rz = self.rz[k]
+                c = camera_struct(cam)
+                status = fn(C.byref(rz._scene_struct), C.byref(c), mode, C.byref(rz.frame), bgv,
+                            C.c_void_p(self.outs[k].data_ptr()), None, None, handles[k])
+                if status:
+                    check(status, "ss_render_frame")
+            for st in self.streams:
+                cur.wait_stream(st)
+            return
         for j, cam in enumerate(cams):
             k = j % self.n_streams
             st, rz = self.streams[k], self.rz[k]

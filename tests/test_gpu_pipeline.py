@@ -31,6 +31,11 @@ def test_pipeline_images_equal_single_stream(n_streams):
     torch.cuda.synchronize()
     for j in range(len(cams)):
         assert np.array_equal(got[j].cpu().numpy(), ref[j]), j
+    # the one-call-per-frame path (no callback): each stream's buffer holds its last frame
+    pipe.render_views([camera_struct(c) for c in cams], (0.1, 0.0, 0.2))
+    torch.cuda.synchronize()
+    for j in range(max(0, len(cams) - n_streams), len(cams)):
+        assert np.array_equal(pipe.outs[j % n_streams].cpu().numpy(), ref[j]), j
     host = [torch.empty((3, 136, 200), dtype=torch.float32).pin_memory() for _ in cams]
     render_views_to_host(pipe, cams, host, (0.1, 0.0, 0.2))
     for j in range(len(cams)):
