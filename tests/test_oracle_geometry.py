@@ -236,3 +236,86 @@ def test_projection_culling_rules():
     for mode, want in [("accutile", [0, 0, 1]), ("snugbox", [0, 0, 1]), ("3sigma", [0, 1, 1])]:
         rec, rect, cnt = oracle.project(sc, cam, mode)
         assert [int(v > 0) for v in cnt] == want, mode
+
+
+JCLAMP = json.load(open(os.path.join(GOLDEN, "jclamp_examples.json")))
+
+
+def _jclamp_scene_cam(case):
+    """The golden's setting: identity view matrix, identity quaternion, cx = W/2, cy = H/2."""
+    cc = case["camera"]
+    vm = np.concatenate([np.eye(3), np.zeros((3, 1))], axis=1).astype(np.float32)
+    cam = synth.Camera(vm, cc["fx"], cc["fy"], cc["width"] / 2.0, cc["height"] / 2.0,
+                       np.zeros(3, np.float32), cc["width"], cc["height"], 0.2, cc["clip"])
+    sc = synth.Scene(np.array([[*case["mean"], 0.8]], np.float32),
+                     np.array([[*case["scale"], 0.0]], np.float32),
+                     np.array([[1, 0, 0, 0]], np.float32), np.zeros((12, 1, 4), np.float32), 3)
+    return sc, cam
+
+
+@pytest.mark.parametrize("case", JCLAMP["cases"], ids=lambda c: c["name"][:30])
+def test_projection_jclamp_hand_derived(case):
+    """R5 (Eq. 4, P:162-166 + the 3D-GS clamp): the J entries use X/Z clamped to
+    +-clip*(W/2)/fx while the projected mean stays unclamped.  The expected Sigma_2D of every
+    case is worked by hand in tests/golden/jclamp_examples.json; a wrong limit (W instead of
+    W/2, fy for fx), a clamped mean or a dropped sign fails at least one case.  Both the
+    float32 contract (or_project) and the float64 forward (or_project_f64) are checked."""
+    sc, cam = _jclamp_scene_cam(case)
+    xx, xy, yy = case["cov2d"]
+    want = np.linalg.inv(np.array([[xx, xy], [xy, yy]], np.float64))
+    rec, rect, cnt = oracle.project(sc, cam, "3sigma")
+    assert rec[0, 11] == 1.0
+    assert np.allclose(rec[0, 0:2], case["xy2d"], rtol=1e-6, atol=1e-4)
+    got = np.array([rec[0, 3], rec[0, 4], rec[0, 5]], np.float64)
+    assert np.allclose(got, [want[0, 0], want[0, 1], want[1, 1]], rtol=2e-5, atol=1e-6 * np.abs(want).max())
+    r64 = oracle.project_f64(sc, cam)
+    assert r64[0, 10] == 1.0
+    assert np.allclose(r64[0, 0:2], case["xy2d"], rtol=1e-12, atol=1e-9)
+    # float64 arithmetic on float32 camera fields (clip = 1.3f is 1.3 - 4.8e-8): 1e-6 relative
+    assert np.allclose(r64[0, 3:6], [want[0, 0], want[0, 1], want[1, 1]], rtol=1e-6, atol=1e-15)
+
+
+def test_projection_clamped_gaussians_numeric_jacobian():
+    """R5 on a real workload view: with clip = 0 EVERY projected Gaussian (also those beyond
+    the 1.3 limit) matches the central-difference Jacobian of the pinhole map; with clip = 1.3
+    the Gaussians beyond the limit match the numeric Jacobian of the pinhole map evaluated at
+    the clamped camera-space point (tx_c Z, ty_c Z, Z) -- the reading 'J at the clamped tx'."""
+    import dataclasses
+    scene, cams = synth.make_workload("mnr360-3m", n=6000)
+    cam = cams[11]
+    V = np.asarray(cam.viewmat, np.float64)
+    Vinv_R = V[:, :3].T
+    for clip in (0.0, 1.3):
+        c2 = dataclasses.replace(cam, clip=clip)
+        rec, rect, cnt = oracle.project(scene, c2, "3sigma")
+        n_clamped = 0
+        for i in range(scene.n):
+            if rec[i, 11] == 0:
+                continue
+            mu = scene.mean_opac[i, :3].astype(np.float64)
+            pc = V[:, :3] @ mu + V[:, 3]
+            tx, ty = pc[0] / pc[2], pc[1] / pc[2]
+            limx, limy = 1.3 * cam.width / 2 / cam.fx, 1.3 * cam.height / 2 / cam.fy
+            clamped = abs(tx) > limx * (1 + 1e-6) or abs(ty) > limy * (1 + 1e-6)
+            if not clamped:
+                continue
+            if clip > 0:  # world point whose camera-space coordinates are the clamped ones
+                pcc = np.array([np.clip(tx, -limx, limx) * pc[2], np.clip(ty, -limy, limy) * pc[2], pc[2]])
+                mu_j = Vinv_R @ (pcc - V[:, 3])
+            else:
+                mu_j = mu
+            q = scene.rot[i].astype(np.float64)
+            q /= np.linalg.norm(q)
+            _, cov = _project_ref(cam, mu_j, scene.scale[i, :3].astype(np.float64), q)
+            # float32 det = xx yy - xy^2 loses ~kappa ulps (kappa = xx yy / det): compare only
+            # where float32 can hold 2e-3 (thin far-off-axis ellipses are skipped, counted)
+            if cov[0, 0] * cov[1, 1] / np.linalg.det(cov) > 1e3:
+                continue
+            conic_ref = np.linalg.inv(cov)
+            nrm = np.abs(conic_ref).max()
+            assert np.allclose(rec[i, 3:6], [conic_ref[0, 0], conic_ref[0, 1], conic_ref[1, 1]], atol=2e-3 * nrm), \
+                (clip, i)
+            n_clamped += 1
+            # the projected mean is never clamped
+            assert abs(rec[i, 0] - (cam.fx * tx + cam.cx)) < 1e-3 + 1e-5 * abs(cam.fx * tx)
+        assert n_clamped > 20, n_clamped
