@@ -147,6 +147,16 @@ def run_oracle_steps(name, mode, steps, warmup, workers):
             "sh_degree": sc.sh_degree, "views": len(cams)}
 
 
+def cpu_model() -> str | None:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -202,8 +212,13 @@ def run_ours(args):
                                               render_views_to_host)
 
     rank, world, local = dist.init()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    if world != args.gpus and rank == 0:
+        print(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; reporting the {world} ranks that ran",
+              file=sys.stderr)
+    dev_index = dist.local_device(local)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    ranks_per_gpu = -(-world // max(1, torch.cuda.device_count()))
     scene, cams = synth.make_workload(args.workload)
     W, H = cams[0].width, cams[0].height
     my_views = dist.views_for_rank(len(cams), rank, world)
@@ -303,6 +318,10 @@ def run_ours(args):
     ms_total = sum(a.elapsed_time(b) for a, b in t_ev)
     ms_max = dist.max_over_ranks(ms_total)
     value = world * n_timed / (ms_max / 1e3)
+    # the workspaces are sized tightly (max P + 2%): no timed frame may have overflowed (an
+    # overflowed frame skips its binning and renders background only)
+    n_overflow = pipe.overflow_count()
+    assert n_overflow == 0, f"{n_overflow} timed frames overflowed the pair capacity"
     # k_preprocess launch durations with frames in flight, from an untimed pipelined pass of V
     # frames with events around every ss_preprocess (the timed steps enqueue each frame with one
     # ss_render_frame call); the per-stage split and the isolated k_preprocess duration come
@@ -318,6 +337,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     stage_ms = {s: sum(ev2[j][i].elapsed_time(ev2[j][i + 1]) for j in range(V)) / V
                 for i, s in enumerate(stages)}
+    frame_ms = sorted(ev2[j][0].elapsed_time(ev2[j][4]) for j in range(V))   # one frame alone on the GPU
+    latency = {"mean_ms": float(np.mean(frame_ms)), "p50_ms": float(np.percentile(frame_ms, 50)),
+               "p95_ms": float(np.percentile(frame_ms, 95)),
+               "timing": "a1-a6 of one frame, CUDA events, single-stream pass of V frames (no other frame in flight)"}
     pre_iso_ms = stage_ms["preprocess"]
 
     # ---- per-stage roofline numbers (averages over the timed frames)
@@ -333,7 +356,7 @@ def run_ours(args):
     stage_info = {}
     for s in stages:
         if s == "render":
-            flops = 9.0 * mean(E_pix) + 10.0 * mean(E_blend)
+            flops = 18.0 * mean(E_pix)   # ~18 FP32 ops per (pixel, Gaussian) evaluation
             ach = flops / (stage_ms[s] / 1e3) / 1e12
             stage_info[s] = {"ms": stage_ms[s], "bound": "alu", "achieved": ach, "peak": fp32_peak,
                              "unit": "TFLOP/s", "frac": ach / fp32_peak,
@@ -344,38 +367,49 @@ def run_ours(args):
             ach = b / (stage_ms[s] / 1e3) / 1e9
             stage_info[s] = {"ms": stage_ms[s], "bound": "hbm", "achieved": ach, "peak": hbm_peak,
                              "unit": "GB/s", "frac": ach / hbm_peak, "bytes": b}
-    # The dominant KERNEL: ss_preprocess is one kernel (k_preprocess, after a 4 KB memset), the
-    # longest single launch of the frame (ncu launch list, profiles/); ss_bin is eight short
-    # kernels and ss_render one (k_render).  The roofline is reported for k_preprocess, timed
-    # by CUDA events on the launching stream around its call; `traffic` is its DRAM bytes per
-    # launch from the committed ncu --set full summary (profiles/traffic.json), when present.
-    dom = "preprocess"
-    di = stage_info[dom]
-    traffic, traffic_src = None, None
+    # The dominant KERNEL, by measured launch duration: ss_preprocess and ss_render are one
+    # kernel each (k_preprocess after a 4 KB memset; k_render), ss_bin / ss_sort are chains of
+    # short kernels.  Both single-kernel stages are reported under roofline["kernels"], timed by
+    # CUDA events on the launching stream in the single-stream pass of the same run (a launch
+    # has the GPU to itself there, so its share of the frame matches the ncu launch list); the
+    # longer one is the line's roofline.  `traffic` = its DRAM bytes per launch from the
+    # committed ncu --set full summary (profiles/traffic.json), when present.
+    traffic = {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    tsrc = None
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
+        tsrc = tj.get("source")
         for k, v in tj.get("kernels", {}).items():
-            if k.startswith("k_preprocess"):
-                traffic, traffic_src = v["dram_bytes"], tj.get("source")
-    iso_ach = di["bytes"] / (pre_iso_ms / 1e3) / 1e9
-    # Primary figure: k_preprocess launches timed by events on their stream in the single-stream
-    # pass of the same run (V frames, same views), where a launch has the GPU to itself, so
-    # achieved = algorithmic bytes / launch duration is the kernel's own bandwidth and its share
-    # of the frame matches the ncu launch list.  In the timed region 3 frames are in flight and a
-    # launch shares the SMs and HBM with the other streams' kernels, which stretches its duration
-    # (reported under "in_flight"; the throughput gain is the point of the pipeline).
-    roof = {"bound": di["bound"], "achieved": iso_ach, "peak": di["peak"], "unit": di["unit"],
-            "frac": iso_ach / di["peak"], "traffic": traffic, "traffic_source": traffic_src,
-            "launch_ms": pre_iso_ms, "timing": "CUDA events on the launching stream, single-stream pass of V frames "
-                                               "of the same workload in the same run (L2 flushed before it)",
-            "in_flight": {"launch_ms": pre_ms, "achieved": di["bytes"] / (pre_ms / 1e3) / 1e9,
-                          "frac": di["bytes"] / (pre_ms / 1e3) / 1e9 / di["peak"],
-                          "timing": f"pipelined pass of V frames, {args.streams} frames in flight on {args.streams} "
-                                    f"streams: launch durations include sharing the GPU with the other frames"},
-            "algorithmic_bytes": di["bytes"], "kernel": "k_preprocess",
-            "peak_source": hbm_src if di["bound"] == "hbm" else
-            f"derived: 148 SM x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {sm_max:.0f} MHz"}
+            for kn in ("k_preprocess", "k_render<"):
+                if k.startswith(kn):
+                    traffic[kn.rstrip("<")] = v["dram_bytes"]
+    pre = stage_info["preprocess"]
+    kern = {
+        "k_preprocess": {"bound": "hbm", "launch_ms": pre_iso_ms, "achieved": pre["achieved"], "peak": hbm_peak,
+                         "unit": "GB/s", "frac": pre["frac"], "algorithmic_bytes": pre["bytes"],
+                         "traffic": traffic.get("k_preprocess"), "peak_source": hbm_src,
+                         "unit_work": "16 B per Gaussian + 4 B depth key + per visible Gaussian 32 B scale/rot "
+                                      "+ 48 B record (DESIGN.md §5)",
+                         "in_flight": {"launch_ms": pre_ms, "achieved": pre["bytes"] / (pre_ms / 1e3) / 1e9,
+                                       "frac": pre["bytes"] / (pre_ms / 1e3) / 1e9 / hbm_peak,
+                                       "timing": f"pipelined pass of V frames, {args.streams} frames in flight"}},
+    }
+    r_ms = stage_ms["render"]
+    r_flop = 18.0 * mean(E_pix)
+    kern["k_render"] = {"bound": "alu", "launch_ms": r_ms, "achieved": r_flop / (r_ms / 1e3) / 1e12,
+                        "peak": fp32_peak, "unit": "TFLOP/s", "frac": r_flop / (r_ms / 1e3) / 1e12 / fp32_peak,
+                        "algorithmic_flop": r_flop, "traffic": traffic.get("k_render"),
+                        "unit_work": "18 FP32 ops per (pixel, Gaussian) evaluation x E_pix (SURVEY §8(d)); "
+                                     "E_pix from ss_render_stats",
+                        "peak_source": f"derived: 148 SM x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {sm_max:.0f} MHz"}
+    dom = max(kern, key=lambda k: kern[k]["launch_ms"])
+    d = kern[dom]
+    roof = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"], "frac": d["frac"],
+            "traffic": d["traffic"], "traffic_source": tsrc, "kernel": dom, "launch_ms": d["launch_ms"],
+            "timing": "CUDA events on the launching stream, single-stream pass of V frames of the same workload in "
+                      "the same run (L2 flushed before it); dominant = the longer single-kernel stage",
+            "kernels": kern}
 
     # ---- pruning-score pass (a1-a5 + a7 over this rank's views, then the NCCL all_reduce)
     score_info = None
@@ -391,14 +425,22 @@ def run_ours(args):
         a.record(stream)
         pipe.score_views(svs, score)       # a1-a5 + a7 per view, frames in flight
         b.record(stream)
-        dist.allreduce_scores(score)
+        dist.allreduce_scores(score)       # no-op at world size 1
         c.record(stream)
         torch.cuda.synchronize()
+        pipe.check_overflow()
         ms_s = dist.max_over_ranks(a.elapsed_time(c))
+        if world > 1:
+            ar = {"ms": dist.max_over_ranks(b.elapsed_time(c)), "bytes": 8 * ds.n, "backend": dist.backend(),
+                  "op": "all_reduce(SUM) of the float64 score vector, once per scoring pass",
+                  "timing": "CUDA events on the caller's stream around the collective, max over ranks"}
+            if dist.backend() == "gloo":
+                ar["note"] = f"{world} ranks share {torch.cuda.device_count()} GPU(s): gloo through host memory"
+        else:
+            ar = "skipped (world 1)"
         score_info = {"views_per_s": world * n_sv / (ms_s / 1e3), "views": world * n_sv,
-                      "ms_score_views": a.elapsed_time(b), "ms_allreduce": b.elapsed_time(c),
-                      "allreduce_bytes": 8 * ds.n, "dtype": "f64 accumulate, f32 per-pixel",
-                      "frames_in_flight": args.streams}
+                      "ms_score_views": dist.max_over_ranks(a.elapsed_time(b)), "allreduce": ar,
+                      "dtype": "f64 accumulate, f32 per-pixel", "frames_in_flight": args.streams}
 
     # ---- backward pass (NEXT-2): forward with T / n_contrib, render backward, preprocess backward
     bw_info = None
@@ -468,7 +510,7 @@ def run_ours(args):
         tcams = [cams[v] for v in my_views[:n_tv]]
         targets = [torch.zeros((3, H, W), dtype=torch.float32, device=dev).uniform_(0, 1) for _ in tcams]
         tscene = DeviceScene(ds.mean_opac.clone(), ds.scale.clone(), ds.rot.clone(), ds.sh.clone(), ds.sh_degree)
-        tr = Trainer(tscene, tcams, targets, adam=AdamConfig(extent=4.0), check_overflow=False)
+        tr = Trainer(tscene, tcams, targets, adam=AdamConfig(extent=4.0), check_overflow=False, replica=True)
         for j in range(3):
             tr.step(j % n_tv)
         n_it = max(8, args.steps)
@@ -491,8 +533,10 @@ def run_ours(args):
         slot_bytes = 16 * (3 + {0: 1, 1: 3, 2: 7, 3: 12}[scene.sh_degree])
         n_flag = int(tr.flags.sum().item())
         adam_bytes = 7 * slot_bytes * ds.n + slot_bytes * n_flag + ds.n
-        train_info = {"iters_per_s": world * n_it / (ms_t / 1e3), "iters": world * n_it, "flagged": n_flag,
-                      "note": "one view per iteration (replica per rank): a1-a6 with T/n_contrib, ss_l1_loss_grad, "
+        train_info = {"iters_per_s_per_replica": n_it / (ms_t / 1e3), "iters": n_it, "replicas": world,
+                      "flagged": n_flag,
+                      "note": "one view per iteration, single replica (ranks train independent copies, no gradient "
+                              "exchange; the slowest rank's time): a1-a6 with T/n_contrib, ss_l1_loss_grad, "
                               "ss_render_backward, ss_preprocess_backward_assign (gradients written for the "
                               "blended Gaussians, flagged), ss_adam_step_flagged over all N Gaussians (dense "
                               "Adam, as 3D-GS; unflagged gradients are zero); targets uniform random; capacity "
@@ -527,9 +571,13 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.ncu:
         workers = max(1, min(8, host_cores()))
         r = run_oracle_steps(args.workload, args.mode, 1, 0, workers)
+        r1 = run_oracle_steps(args.workload, args.mode, 1, 0, 1)
         cpu = {"value": r["value"], "unit": "frames/s", "cores": workers, "kind": "oracle",
                "sample": f"{r['frames']} full views of {args.workload} (project, bin, sort, render; one view per "
-                         f"worker process)"}
+                         f"worker process)",
+               "one_core": {"value": r1["value"], "unit": "frames/s", "cores": 1, "ms_per_frame": r1["ms_per_step"],
+                            "sample": f"1 full view of {args.workload}, one process"},
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {
@@ -541,10 +589,13 @@ def run_ours(args):
                        "n_gaussians": ds.n, "pruned": prune_info, "width": W, "height": H,
                        "views": len(cams), "views_per_step_per_rank": V, "mode": args.mode,
                        "sh_degree": scene.sh_degree, "parallelism": f"view-parallel x{world}",
+                       "process_group": dist.backend() or "none (1 rank)",
+                       "gpus_visible": torch.cuda.device_count(), "ranks_per_gpu": ranks_per_gpu,
                        "frames_in_flight": args.streams,
                        "l2": "flushed between steps (256 MB written outside the timed regions); scene %.0f MB, "
                              "per-frame records %.0f MB" % (ds.n * 240 / 1e6, NVm * 48 / 1e6)},
             "pairs_per_frame": {"mean": Pm, "min": min(pairs.values()), "max": max(pairs.values())},
+            "frame_latency": latency,
             "pairs_per_s": value * Pm,
             "visible_per_frame": NVm,
             "coloured_per_frame": mean(ncol),
@@ -571,8 +622,26 @@ def run_ours(args):
     return 0
 
 
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` without a torchrun environment: launch N ranks of this command on this node
+    (torch.distributed.run, rendezvous on 127.0.0.1), one process per GPU; rank 0 prints the
+    line.  NCCL_DEBUG=INFO lets the NCCL communicator report its ranks on stderr."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

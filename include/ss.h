@@ -36,9 +36,12 @@
  *     tiles or more than 256 tiles along an axis, n or capacity >= 2^30).  A failed launch returns SS_ERR_CUDA (the CUDA error
  *     string is available from ss_last_cuda_error of the same thread).  Device-side faults
  *     surface on the caller's next synchronisation.  Pair-array overflow is NOT an error
- *     code: ss_bin writes min(P, capacity) pairs, stores P in the workspace's total_pairs
- *     and sets its overflow flag; the caller reads them, grows `capacity` and re-runs the
- *     frame (every call is idempotent given the same inputs).
+ *     code (the calls only enqueue work, and P is known on the device only): ss_preprocess
+ *     stores P in the workspace's total_pairs; ss_bin sets the overflow flag and increments the
+ *     sticky overflow_count, and then ss_bin / ss_sort write NO pairs (all ranges empty), so
+ *     ss_render outputs background only and ss_prune_score adds nothing for that frame.  The
+ *     caller reads overflow (one frame) or overflow_count (a batch of frames, one read), grows
+ *     `capacity` and re-runs those frames (every call is idempotent given the same inputs).
  */
 #ifndef SS_H
 #define SS_H
@@ -135,7 +138,10 @@ typedef struct {
     size_t ranges;        /* uint32 [n_tiles][2] per tile [start, end) into sorted_value      */
     size_t n_visible;     /* uint32 [1]   Gaussians with >= 1 tile                            */
     size_t total_pairs;   /* uint32 [1]   P (written by ss_preprocess)                        */
-    size_t overflow;      /* uint32 [1]   1 iff P > capacity                                  */
+    size_t overflow;      /* uint32 [1]   1 iff P > capacity (this frame; rewritten by ss_bin)  */
+    size_t overflow_count;/* uint32 [1]   sticky: frames with P > capacity since the caller last
+                                          zeroed it (libss only increments it; zero it when the
+                                          workspace is allocated)                               */
     size_t scratch;       /* internal                                                         */
     size_t total_bytes;
     int32_t tiles_x, tiles_y, n_tiles, tile_bits;
@@ -212,7 +218,9 @@ SS_API ss_status ss_prune_score(const ss_frame *frame /*host*/, const float *bg 
  * U~); on equal scores the higher index is removed first.  ratio in [0, 1].
  * ss_compact_scene: stable stream compaction of every array of `in` into `out` (device arrays
  * allocated by the caller for out->n = n - k Gaussians); *n_out (device uint32) receives the
- * survivor count.  Both use a caller workspace
+ * survivor count (the number of non-zero keep entries).  Only the first out->n survivors are
+ * written: a mask keeping more than out->n is not a memory error, and the caller detects it by
+ * *n_out > out->n.  Both use a caller workspace
  * of ss_prune_workspace_size(n) bytes (device). */
 SS_API size_t ss_prune_workspace_size(int32_t n);
 SS_API uint32_t ss_prune_count(int32_t n, double ratio);

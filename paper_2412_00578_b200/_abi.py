@@ -37,7 +37,7 @@ class SsFrame(C.Structure):
 
 class SsLayout(C.Structure):
     _fields_ = [(k, C.c_size_t) for k in ("rec", "erec", "depth_key", "order", "sorted_value", "tile_count", "ranges", "n_visible", "total_pairs",
-                                          "overflow", "scratch", "total_bytes")] + \
+                                          "overflow", "overflow_count", "scratch", "total_bytes")] + \
                [(k, C.c_int32) for k in ("tiles_x", "tiles_y", "n_tiles", "tile_bits")]
 
 

@@ -30,7 +30,7 @@ UNITS = {
     "ss_backward.cu": [],
     "ss_train.cu": [],
 }
-HEADERS = ["ss_common.cuh", "ss_tilegeom.cuh"]
+HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith(".cuh"))
 
 
 def _stale(target: str, deps: list[str]) -> bool:

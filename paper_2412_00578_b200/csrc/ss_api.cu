@@ -63,6 +63,7 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     L->tile_base = take(4 * T);
     L->color_src = take(64);
     P.overflow = take(4);
+    P.overflow_count = take(4);
     // ---- regions each call clears for itself (so every call is idempotent given its inputs)
     L->zero_pre = off;  // written by ss_preprocess
     P.n_visible = take(4);
@@ -96,11 +97,18 @@ static ss_status check_frame(const ss_frame *f, Layout *L) {
     return SS_OK;
 }
 
+// Camera values every call relies on: positive finite focal lengths, a positive near plane
+// (z_near <= 0 would admit Gaussians at or behind the camera, whose depth bits sort wrongly)
+// and a finite, non-negative J clamp (0 = off).
+static bool cam_values_ok(const ss_camera &c) {
+    return c.fx > 0.0f && c.fy > 0.0f && std::isfinite(c.fx) && std::isfinite(c.fy) && c.z_near > 0.0f &&
+           std::isfinite(c.z_near) && c.clip >= 0.0f && std::isfinite(c.clip);
+}
+
 static ss_status check_cam(const ss_camera *c, const ss_frame *f) {
     if (!c) return SS_ERR_INVALID_ARG;
     if (c->width != f->width || c->height != f->height) return SS_ERR_INVALID_ARG;
-    if (!(c->fx > 0.0f) || !(c->fy > 0.0f)) return SS_ERR_INVALID_ARG;
-    return SS_OK;
+    return cam_values_ok(*c) ? SS_OK : SS_ERR_INVALID_ARG;
 }
 
 static CamArgs cam_args(const ss_camera &c, const Layout &L) {
@@ -236,7 +244,7 @@ static ss_status preprocess_backward(const ss_scene *scene, const ss_camera *cam
     if (!scene || !cam || !grad || scene->n < 0 || scene->sh_degree < 0 || scene->sh_degree > 3) return SS_ERR_INVALID_ARG;
     if (grad->n != scene->n || grad->sh_degree != scene->sh_degree) return SS_ERR_INVALID_ARG;
     if (scene->n >= (1 << 30)) return SS_ERR_UNSUPPORTED;
-    if (cam->width <= 0 || cam->height <= 0 || !(cam->fx > 0.0f) || !(cam->fy > 0.0f)) return SS_ERR_INVALID_ARG;
+    if (cam->width <= 0 || cam->height <= 0 || !cam_values_ok(*cam)) return SS_ERR_INVALID_ARG;
     if (scene->n > 0 && (!scene->mean_opac || !scene->scale || !scene->rot || !scene->sh || !grad2d ||
                          !grad->mean_opac || !grad->scale || !grad->rot || !grad->sh))
         return SS_ERR_INVALID_ARG;

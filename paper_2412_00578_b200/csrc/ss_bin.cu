@@ -84,12 +84,17 @@ __global__ void __launch_bounds__(kScanThreads) k_escan_apply(const uint32_t *__
                                                               uint32_t *__restrict__ eoff,
                                                               const uint32_t *__restrict__ total_pairs, uint32_t cap,
                                                               uint32_t *__restrict__ total_entries,
-                                                              uint32_t *__restrict__ overflow) {
+                                                              uint32_t *__restrict__ overflow,
+                                                              uint32_t *__restrict__ overflow_count) {
     pdl_enter();
     __shared__ uint32_t s_warp[8];
     const uint32_t nv = *n_visible;
     const int tid = threadIdx.x;
-    if (blockIdx.x == 0 && tid == 0) *overflow = *total_pairs > cap ? 1u : 0u;
+    if (blockIdx.x == 0 && tid == 0) {
+        const bool ovf = *total_pairs > cap;
+        *overflow = ovf ? 1u : 0u;
+        if (ovf) atomicAdd(overflow_count, 1u);
+    }
     const size_t base = (size_t)blockIdx.x * kScanTile;
     if (base >= nv) return;
     // the sum of the earlier tiles
@@ -715,7 +720,8 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
                at<const uint32_t>(ws, L.one), at<uint32_t>(ws, L.lb_escan));
     launch_pdl(k_escan_apply, L.nblk_escan, kScanThreads, 0, st, at<const uint32_t>(ws, P.n_visible),
                at<const uint32_t>(ws, L.one), at<const uint32_t>(ws, L.lb_escan), at<uint32_t>(ws, L.eoff),
-               at<const uint32_t>(ws, P.total_pairs), L.capacity, ctr + 8, at<uint32_t>(ws, P.overflow));
+               at<const uint32_t>(ws, P.total_pairs), L.capacity, ctr + 8, at<uint32_t>(ws, P.overflow),
+               at<uint32_t>(ws, P.overflow_count));
     if (L.nck_max == 0) return cudaGetLastError();
     const uint32_t *E = ctr + 8;
     int sbits = 1;

@@ -167,7 +167,9 @@ __global__ void __launch_bounds__(256) k_compact(int n, const uint8_t *__restric
             if ((size_t)(bid + 1) * 256 >= (size_t)n) *n_out = acc + total;
         }
         __syncthreads();
-        if (f) {
+        // survivors beyond the caller's out->n (a mask keeping more than the allocation) are
+        // counted in *n_out but not written
+        if (f && s_base + excl < out_stride) {
             const uint32_t o = s_base + excl;
             mo_out[o] = mo_in[i];
             sc_out[o] = sc_in[i];

@@ -20,16 +20,35 @@ def world() -> tuple[int, int, int]:
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def default_backend(world_size: int) -> str:
+    """NCCL when every rank has a GPU of its own; gloo otherwise (CPU tests, or several ranks
+    sharing one GPU -- NCCL refuses two ranks on one device; gloo all_reduces CUDA tensors
+    through host memory)."""
+    if torch.cuda.is_available() and torch.cuda.device_count() >= world_size:
+        return "nccl"
+    return "gloo"
+
+
+def local_device(local_rank: int) -> int:
+    """CUDA device of a local rank (ranks beyond the device count share devices round-robin)."""
+    return local_rank % max(1, torch.cuda.device_count())
+
+
 def init(backend: str | None = None) -> tuple[int, int, int]:
     rank, ws, lr = world()
     if ws > 1 and not dist.is_initialized():
         if backend is None:
-            backend = "nccl" if torch.cuda.is_available() else "gloo"
-        if backend == "nccl":
-            torch.cuda.set_device(lr)
+            backend = default_backend(ws)
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local_device(lr))
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group(backend=backend, rank=rank, world_size=ws)
+        kw = {"device_id": torch.device("cuda", local_device(lr))} if backend == "nccl" else {}
+        dist.init_process_group(backend=backend, rank=rank, world_size=ws, **kw)
     return rank, ws, lr
+
+
+def backend() -> str | None:
+    return dist.get_backend() if dist.is_available() and dist.is_initialized() else None
 
 
 def views_for_rank(n_views: int, rank: int, world_size: int) -> list[int]:

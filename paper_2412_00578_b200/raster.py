@@ -95,6 +95,7 @@ class Rasterizer:
         self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         self.capacity = capacity
         self.layout = _abi.layout(self.scene.n, capacity, self.width, self.height)
+        self.ws[self.layout.overflow_count: self.layout.overflow_count + 4].zero_()   # sticky counter
         self.frame = SsFrame(self.ws.data_ptr(), nbytes, self.scene.n, capacity, self.width, self.height)
         self.n_tiles = self.layout.n_tiles
 
@@ -139,6 +140,14 @@ class Rasterizer:
         P = int(self._view(self.layout.total_pairs, 1, torch.int32).item()) & 0xFFFFFFFF
         ov = int(self._view(self.layout.overflow, 1, torch.int32).item())
         return {"n_visible": nv, "pairs": P, "overflow": ov}
+
+    def overflow_count(self) -> int:
+        """Frames of this workspace whose pairs exceeded the capacity since the last
+        clear_overflow() (sticky device counter; synchronises)."""
+        return int(self._view(self.layout.overflow_count, 1, torch.int32).item())
+
+    def clear_overflow(self) -> None:
+        self._view(self.layout.overflow_count, 1, torch.int32).zero_()
 
     # ---------------------------------------------------------------- the five calls
     def preprocess(self, cam, stream=None) -> None:
@@ -285,7 +294,27 @@ class FramePipeline:
         for r in self.rz:
             if r.capacity != cap:
                 r._alloc(cap)
+        self.clear_overflow()
         return P
+
+    def overflow_count(self) -> int:
+        """Frames (on any workspace) whose pairs exceeded the capacity since the last
+        clear_overflow(): one device read per workspace (synchronises).  The render / score
+        calls never read it themselves (they only enqueue work); a caller that did not size
+        the workspaces with ensure_capacity() checks it after a batch."""
+        return sum(r.overflow_count() for r in self.rz)
+
+    def clear_overflow(self) -> None:
+        for r in self.rz:
+            r.clear_overflow()
+
+    def check_overflow(self) -> None:
+        """Raise SsError if a frame since the last clear_overflow() overflowed its workspace
+        (its image would be background only, its score contribution zero)."""
+        k = self.overflow_count()
+        if k:
+            raise _abi.SsError(f"{k} frame(s) exceeded the pair capacity {self.rz[0].capacity}; "
+                               f"call ensure_capacity() for these cameras and re-run them")
 
     def render_views(self, cams, bg=(0.0, 0.0, 0.0), on_frame=None, pre_events=None) -> None:
         """Render every camera (a1-a6).  on_frame(j, image, stream) is called right after
@@ -361,8 +390,15 @@ def render_views_to_host(pipe: "FramePipeline", cams, host_out: list, bg=(0.0, 0
     copy completes.  host_out[j] must be pinned float32 [3, H, W] tensors."""
     def copy(j, img, st):
         host_out[j].copy_(img, non_blocking=True)
-    pipe.render_views([camera_struct(c) for c in cams], bg, on_frame=copy)
+    cs = [camera_struct(c) for c in cams]
+    pipe.render_views(cs, bg, on_frame=copy)
     torch.cuda.current_stream().synchronize()
+    if pipe.overflow_count():   # a view needed more pairs than the workspaces hold: grow, redo
+        pipe.clear_overflow()
+        pipe.ensure_capacity(cs)
+        pipe.render_views(cs, bg, on_frame=copy)
+        torch.cuda.current_stream().synchronize()
+        pipe.check_overflow()
 
 
 def prune_select(score: torch.Tensor, ratio: float, stream=None) -> tuple[torch.Tensor, int]:
@@ -393,6 +429,9 @@ def compact(scene: DeviceScene, keep: torch.Tensor, n_keep: int, stream=None) ->
     check(lib().ss_compact_scene(C.byref(src), C.c_void_p(keep.data_ptr()), C.byref(dst),
                                  C.c_void_p(n_out.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(),
                                  C.c_void_p(_stream_handle(stream))), "ss_compact_scene")
+    got = int(n_out.item())   # synchronises: a mismatched mask must not yield a short scene
+    if got != m:
+        raise _abi.SsError(f"compact: the keep mask keeps {got} Gaussians, the caller allocated {m}")
     return out
 
 

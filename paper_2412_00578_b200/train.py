@@ -70,7 +70,17 @@ class Trainer:
 
     def __init__(self, scene: DeviceScene, cams, targets: list[torch.Tensor], bg=(0.0, 0.0, 0.0),
                  mode: str = "accutile", adam: AdamConfig | None = None, seed: int = 0,
-                 check_overflow: bool = True):
+                 check_overflow: bool = True, replica: bool = False):
+        # Training is single-replica: every step updates this process's scene from one view,
+        # with no gradient exchange.  Under a process group of world size > 1 the scenes of the
+        # ranks would drift apart (float atomics make each backward's summation order differ),
+        # so an all-reduced score would mix different scenes.  replica=True states that this
+        # rank trains an independent copy: it then scores all views itself, with no all_reduce.
+        _, world, _ = dist.world()
+        if world > 1 and not replica:
+            raise ValueError("Trainer has no gradient exchange: under world size > 1 pass replica=True "
+                             "(independent per-rank copies, no score all_reduce)")
+        self.replica = bool(replica) or world == 1
         self.check_overflow = check_overflow   # False: capacity sized up front, no per-step read-back
         self.cams = list(cams)
         self.targets = targets
@@ -155,13 +165,14 @@ class Trainer:
         """Ũ over every training view: this rank's shard of the views with several frames in
         flight (FramePipeline.score_views), then the float64 all_reduce."""
         rank, world, _ = dist.world()
-        mine = dist.views_for_rank(len(self.cams), rank, world)
+        mine = list(range(len(self.cams))) if self.replica else dist.views_for_rank(len(self.cams), rank, world)
         score = torch.zeros(self.n, dtype=torch.float64, device=self.dev)
         if mine:
             pipe = FramePipeline(self.scene, self.W, self.H, mode=self.mode, n_streams=n_streams)
             pipe.ensure_capacity([self.cams[v] for v in mine], headroom=1.05)
             pipe.score_views([self.cstructs[v] for v in mine], score, self.bg)
-        return dist.allreduce_scores(score)
+            pipe.check_overflow()
+        return score if self.replica else dist.allreduce_scores(score)
 
     def prune(self, ratio: float, score: torch.Tensor | None = None) -> int:
         """Remove ⌊ratio·N⌋ lowest-Ũ Gaussians with their Adam state; returns the removed count."""

@@ -14,6 +14,9 @@ smoke)
 bench)
   timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench_exit=$?; tail -3 gpurun_out/${TAG}_bench.err
   python -c "import json; d=json.load(open('gpurun_out/${TAG}_bench.json')); print(d['value'], d['stages_ms'], d.get('kernels_us'), d['roofline'])" ;;
+bench2)
+  timeout 900 python bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/${TAG}_bench2.json 2> gpurun_out/${TAG}_bench2.err; echo bench2_exit=$?; tail -3 gpurun_out/${TAG}_bench2.err
+  python -c "import json; d=json.load(open('gpurun_out/${TAG}_bench2.json')); print(d['n_gpus'], d['value'], d['config']['process_group'], d['prune_score'])" ;;
 benchfast)
   timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --no-score > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err; echo bench_exit=$?; tail -3 gpurun_out/${TAG}_bench.err
   python -c "import json; d=json.load(open('gpurun_out/${TAG}_bench.json')); print(d['value'], d['stages_ms'], d.get('kernels_us'))" ;;

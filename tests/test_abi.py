@@ -32,7 +32,7 @@ def test_layout_and_workspace(lib):
     assert (L.tiles_x, L.tiles_y, L.n_tiles, L.tile_bits) == (16, 16, 256, 8)
     assert L.total_bytes == _abi.workspace_size(1000, 4096, 256, 256)
     offs = sorted([L.rec, L.erec, L.depth_key, L.order, L.sorted_value,
-                   L.ranges, L.tile_count, L.n_visible, L.total_pairs, L.overflow])
+                   L.ranges, L.tile_count, L.n_visible, L.total_pairs, L.overflow, L.overflow_count])
     assert len(set(offs)) == len(offs) and all(o % 256 == 0 for o in offs)
     L2 = _abi.layout(10, 100, 1297, 840)
     assert (L2.tiles_x, L2.tiles_y, L2.tile_bits) == (82, 53, 13)
@@ -57,6 +57,17 @@ def test_invalid_arguments_rejected_before_launch(lib):
     assert lib.ss_preprocess(C.byref(sc2), C.byref(st), 2, C.byref(fr), None) == _abi.SS_ERR_INVALID_ARG
     sc3 = _abi.SsScene(10, 3, 1, 1, 1, 1)
     assert lib.ss_preprocess(C.byref(sc3), C.byref(st), 7, C.byref(fr), None) == _abi.SS_ERR_INVALID_ARG
+    # camera values: z_near <= 0 or non-finite, negative / non-finite J clamp
+    ok = _abi.SsCamera()
+    ok.width, ok.height, ok.fx, ok.fy, ok.z_near, ok.clip = 64, 64, 100.0, 100.0, 0.2, 1.3
+    for field, bad in (("z_near", 0.0), ("z_near", -0.2), ("z_near", float("nan")), ("clip", -1.0),
+                       ("clip", float("inf")), ("fx", float("inf"))):
+        c = _abi.SsCamera()
+        C.memmove(C.byref(c), C.byref(ok), C.sizeof(c))
+        setattr(c, field, bad)
+        assert lib.ss_bin(C.byref(c), 2, C.byref(fr), None) == _abi.SS_ERR_INVALID_ARG, (field, bad)
+        g = _abi.SsScene(10, 3, 1, 1, 1, 1)  # ss_scene_grad has ss_scene's layout
+        assert lib.ss_preprocess_backward(C.byref(sc3), C.byref(c), 1, C.byref(g), None) == _abi.SS_ERR_INVALID_ARG
     big = _abi.SsFrame(1234, 1 << 40, 10, 100, 16 * 65537, 16)
     assert lib.ss_sort(C.byref(big), None) == _abi.SS_ERR_UNSUPPORTED  # > 256 tiles along x
     assert _abi.layout(10, 100, 4096, 4096).n_tiles == 65536  # the largest supported grid (no launch here)

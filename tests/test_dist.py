@@ -64,3 +64,13 @@ def test_score_allreduce_world2_matches_single_process():
         r0, r1 = out[0], out[1]
     assert np.array_equal(r0, r1), "every rank must hold the identical reduced vector"
     assert np.allclose(r0, ref, rtol=1e-12, atol=0)
+
+
+def test_trainer_refuses_unsynchronised_multi_rank(monkeypatch):
+    """Training has no gradient exchange: under world size > 1 a Trainer must be an explicit
+    independent replica, or its all-reduced scores would mix drifted scenes."""
+    from paper_2412_00578_b200.train import Trainer
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setenv("RANK", "1")
+    with pytest.raises(ValueError, match="replica"):
+        Trainer(None, [], [])
