@@ -2,10 +2,14 @@
 // NEXT-2 render backward.
 //
 // One CTA per 16x16 tile, one thread per pixel ("parallelized across pixels").  The
-// tile's depth-ordered Gaussian ids are consumed in batches of kBatch = 128: one thread per
-// slot gathers the 48 B record into shared memory (computing the view-dependent colour on
-// first use, ss_color.cuh), then every still-active pixel walks the batch.  Before every batch
-// the active pixels are compacted onto the lowest threads; a CTA stops as soon as none is left.
+// tile's depth-ordered Gaussian ids are consumed in batches of kBatch = 128.  k_render stages
+// them asynchronously: while the pixels walk batch b, one thread per slot has batch b+1's
+// 48 B records in flight (cp.async, LDGSTS) and batch b+2's ids loaded; a landed batch is
+// transposed into a pair-interleaved layout (computing the view-dependent colour on first use,
+// ss_color.cuh) so that the q / alpha chain of two consecutive Gaussians runs on the packed
+// FP32 pipe (FFMA2 / FMUL2 / FADD2).  Before every batch the active pixels are compacted onto
+// the lowest threads (two barriers per batch); a CTA stops as soon as none is left.  The
+// score / backward / stats kernels gather synchronously (load_batch).
 //
 // Arithmetic contract: the alpha-skip decision q <= t (alpha >= 1/255, Eq. 9)
 // uses the pinned chain u = fma(a, dx, (2b) dy); q = fma(dx, u, (c dy) dy) with explicit
@@ -17,6 +21,13 @@ namespace ss {
 namespace {
 
 constexpr int kBatch = 128;
+#ifndef SS_RENDER_MINB
+#define SS_RENDER_MINB 6  // k_render CTAs per SM (register budget 40)
+#endif
+#ifndef SS_RENDER_UNROLL
+#define SS_RENDER_UNROLL 2
+#endif
+constexpr int kRenderUnroll = SS_RENDER_UNROLL;  // pairs per k_render loop iteration
 
 // Shared-memory batch of gathered records, split by use: the per-warp culling box, the conic
 // (skip test), the colour.
@@ -86,85 +97,213 @@ __device__ __forceinline__ uint32_t compact_active(bool active, PixState &st, ui
     return n_active;
 }
 
+// ---------------------------------------------------------------- staged batches (k_render)
+// Records of batch b+1 are gathered with cp.async (LDGSTS, 3 x 16 B per slot, L2 path) into a
+// raw double buffer while the pixels walk batch b; the ids are loaded two batches ahead.  When
+// a batch has landed its loader thread transposes its slot into structure-of-arrays form
+// (computing a pending colour, ss_color.cuh), so that one 128-bit shared load gives a field of
+// four consecutive Gaussians and consecutive pairs feed the packed FP32 pipe (f32x2).
+struct RawBatch {
+    float4 q[3 * kBatch];  // records as gathered: q0, q1, q2 per slot
+};
+// Pair-interleaved (AoSoA) layout: Gaussians 2p and 2p+1 share 20 floats, so that one 128-bit
+// shared load gives two fields of the pair as two f32x2 operands:
+//   [-x0 -x1 -y0 -y1] [a0 a1 2b0 2b1] [c0 c1 t0 t1] [s0 s1 r0 r1] [g0 g1 bl0 bl1]
+struct SoaBatch {
+    float4 v[kBatch / 2][5];
+};
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Slot threadIdx.x (< kBatch) of a batch: issue the gather of Gaussian g's record.
+__device__ __forceinline__ void stage_gather(RawBatch &raw, const float4 *__restrict__ rec, uint32_t g, bool valid) {
+    if (valid) {
+        const float4 *src = rec + 3 * (size_t)g;
+        cp_async16(&raw.q[3 * threadIdx.x + 0], src + 0);
+        cp_async16(&raw.q[3 * threadIdx.x + 1], src + 1);
+        cp_async16(&raw.q[3 * threadIdx.x + 2], src + 2);
+    }
+}
+
+// Slot threadIdx.x (< kBatch): raw record -> pair-interleaved layout (padding slots never
+// contribute: q <= -inf is false); a pending colour is computed here and stored back.
+__device__ __forceinline__ void stage_transpose(SoaBatch &s, const RawBatch &raw, const float4 *rec, uint32_t g,
+                                                bool valid, const ColorSrc &cs) {
+    const int k = threadIdx.x;
+    float f[10];
+    if (valid) {
+        const float4 q0 = raw.q[3 * k + 0], q1 = raw.q[3 * k + 1];
+        float4 q2 = raw.q[3 * k + 2];
+        if (q2.x == 0.0f) {  // pending colour: computed by this gather (the same value every time)
+            const float3 c = sh_color(cs, g);
+            q2 = make_float4(1.0f, c.x, c.y, c.z);
+            __stcg(const_cast<float4 *>(rec) + 3 * (size_t)g + 2, q2);
+        }
+        f[0] = -q0.x; f[1] = -q0.y; f[2] = q0.z; f[3] = q0.w + q0.w; f[4] = q1.x;
+        f[5] = q1.y; f[6] = q1.z; f[7] = q2.y; f[8] = q2.z; f[9] = q2.w;
+    } else {
+        f[0] = f[1] = 0.0f; f[2] = 1.0f; f[3] = 0.0f; f[4] = 1.0f;
+        f[5] = __int_as_float(0xff800000); f[6] = f[7] = f[8] = f[9] = 0.0f;
+    }
+    float *dst = reinterpret_cast<float *>(&s.v[k >> 1][0]) + (k & 1);
+#pragma unroll
+    for (int j = 0; j < 10; ++j) dst[2 * j] = f[j];
+}
+
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float ex2_approx(float x) {
+    float e;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
+    return e;
+}
+
 template <bool NC>  // NC: track the last blended list entry per pixel (out_ncontrib requested)
-__global__ void __launch_bounds__(256, 6) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
+__global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
                                                 const float4 *__restrict__ rec, int W, int H, int tiles_x, float bg0,
                                                 float bg1, float bg2, float *__restrict__ out_rgb,
                                                 float *__restrict__ out_T, uint32_t *__restrict__ out_nc,
         const ColorSrc *__restrict__ csp) {
     pdl_enter();
     const ColorSrc cs = *csp;
-    __shared__ Batch s;
+    __shared__ __align__(16) RawBatch raw[2];
+    __shared__ __align__(16) SoaBatch s;
     __shared__ PixState st;
     __shared__ uint32_t s_warp[8];
     const int tile = blockIdx.x;
+    const int tid = threadIdx.x;
     int mpx, mpy;
-    tile_pixel(tile, tiles_x, threadIdx.x, mpx, mpy);
+    tile_pixel(tile, tiles_x, tid, mpx, mpy);
     const bool inside = mpx < W && mpy < H;
     const uint2 range = ranges[tile];
-    st.T[threadIdx.x] = 1.0f;
-    st.C0[threadIdx.x] = st.C1[threadIdx.x] = st.C2[threadIdx.x] = 0.0f;
-    st.last[threadIdx.x] = 0;
-    st.done[threadIdx.x] = inside ? 0 : 1;
-    for (uint32_t start = range.x; start < range.y; start += kBatch) {
-        __syncthreads();
-        const uint32_t n_active = compact_active(!st.done[threadIdx.x], st, s_warp);
+    st.T[tid] = 1.0f;
+    st.C0[tid] = st.C1[tid] = st.C2[tid] = 0.0f;
+    st.last[tid] = 0;
+    // ids of batches 0 and 1 of this slot; batch 0 gathered before the loop
+    const bool loader = tid < kBatch;
+    uint32_t g_cur = 0, g_nxt = 0;
+    if (loader) {
+        const uint32_t j0 = range.x + tid, j1 = j0 + kBatch;
+        g_cur = j0 < range.y ? __ldg(vals + j0) : 0u;
+        g_nxt = j1 < range.y ? __ldg(vals + j1) : 0u;
+        stage_gather(raw[0], rec, g_cur, j0 < range.y);
+    }
+    cp_async_commit();
+    // Pixel compaction, two barriers per batch: every thread carries the pixel it walked (my_pp)
+    // and whether it is still active (my_act); per-warp counts of the active ones are published
+    // with the barrier that ends the walk, and the next list (stable: pixel-index order) is
+    // written from registers.  Warps whose pixels have all terminated stop issuing.
+    uint32_t my_pp = (uint32_t)tid;
+    bool my_act = inside;
+    uint32_t bal = __ballot_sync(0xffffffffu, my_act);
+    if ((tid & 31) == 0) s_warp[tid >> 5] = __popc(bal);
+    int buf = 0;
+    for (uint32_t start = range.x; start < range.y; start += kBatch, buf ^= 1) {
+        __syncthreads();  // the previous walk is done: s, raw[buf ^ 1] free; warp counts visible
+        uint32_t n_active = 0, pos = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            const uint32_t c = s_warp[w];
+            pos += w < (tid >> 5) ? c : 0u;
+            n_active += c;
+        }
         if (n_active == 0) break;
-        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr, cs);
-        __syncthreads();
-        if (threadIdx.x < n_active) {
-            const int pp = st.list[threadIdx.x];
+        if (my_act) st.list[pos + __popc(bal & ((1u << (tid & 31)) - 1u))] = (uint16_t)my_pp;
+        uint32_t g_after = 0;
+        if (loader) {
+            const uint32_t j1 = start + kBatch + tid, j2 = j1 + kBatch;
+            stage_gather(raw[buf ^ 1], rec, g_nxt, j1 < range.y);           // batch b+1, in flight
+            g_after = j2 < range.y ? __ldg(vals + j2) : 0u;                 // id of batch b+2
+        }
+        cp_async_commit();
+        cp_async_wait<1>();  // this thread's gathers of batch b have landed
+        if (loader) stage_transpose(s, raw[buf], rec, g_cur, start + tid < range.y, cs);
+        g_cur = g_nxt;
+        g_nxt = g_after;
+        __syncthreads();  // batch b staged, the list written
+        my_act = false;
+        if (tid < n_active) {
+            const int pp = st.list[tid];
             int px, py;
             tile_pixel(tile, tiles_x, pp, px, py);
-            const float fpx = (float)px, fpy = (float)py;
+            const float2 FX = f2((float)px), FY = f2((float)py);
             float T = st.T[pp], C0 = st.C0[pp], C1 = st.C1[pp], C2 = st.C2[pp];
             uint32_t last = st.last[pp];
             bool done = false;
-            // the batch is walked in groups of 4; the padding slots after the last Gaussian
-            // never contribute, so no per-Gaussian bound check is needed
-            const int cnt = ((int)min((uint32_t)kBatch, range.y - start) + 3) & ~3;
+            // pairs of consecutive Gaussians over the padded batch (padding slots never
+            // contribute).  The q / alpha chain of a pair runs on the packed FP32 pipe (f32x2;
+            // each half rounded as the scalar op, so q is bit-identical to the oracle's chain,
+            // R15).  A non-contributing Gaussian gets alpha = 0, which leaves T unchanged.  T is
+            // monotone, so when T after the pair is >= 1e-4 neither Gaussian terminates and both
+            // blend (the common case: one test per pair); otherwise the pair is taken in order.
+            // The colour sums stay sequential (C += c alpha T in list order), so the image is
+            // bit-identical to a one-by-one walk: AccuTile and SnugBox renders stay bitwise equal
+            // (their lists differ only by Gaussians with alpha = 0 everywhere in the tile).
+            const int cnt = ((int)min((uint32_t)kBatch, range.y - start) + 1) & ~1;
             const uint32_t base = start - range.x + 1;
-            // branch-free blend: a non-contributing Gaussian gets alpha = 0, which leaves T and
-            // C bit-identical (T * 1 = T, fma(c, 0, C) = C), so only termination branches
-            for (int k4 = 0; k4 < cnt && !done; k4 += 4)
-#pragma unroll
-            for (int k = k4; k < k4 + 4; ++k) {
-                const float4 bx = s.box[k];
-                const float4 cn = s.con[k];
-                const float4 cl = s.col[k];
-                const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
-                const bool contrib = q <= cn.w;  // alpha >= 1/255 (Eq. 9, R15)
-                const float alpha = contrib ? alpha_of(q, cl.w) : 0.0f;
-                const float Tn = T * (1.0f - alpha);
-                if (Tn < 1e-4f) {  // R16: stop before blending (never for alpha = 0: T >= 1e-4)
+#pragma unroll kRenderUnroll
+            for (int k = 0; k < cnt; k += 2) {
+                const float4 *v = s.v[k >> 1];
+                const float4 v0 = v[0], v1 = v[1], v2 = v[2];
+                // q = (p - mu)^T Sigma^-1 (p - mu): dx = px - x, u = fma(a, dx, 2b dy),
+                // q = fma(dx, u, (c dy) dy)
+                const float2 dx = __fadd2_rn(FX, make_float2(v0.x, v0.y));
+                const float2 dy = __fadd2_rn(FY, make_float2(v0.z, v0.w));
+                const float2 u = __ffma2_rn(make_float2(v1.x, v1.y), dx, __fmul2_rn(make_float2(v1.z, v1.w), dy));
+                const float2 q = __ffma2_rn(dx, u, __fmul2_rn(__fmul2_rn(make_float2(v2.x, v2.y), dy), dy));
+                const float2 ql = __fmul2_rn(q, f2(-0.72134752044448170f));  // -q/2 in log2 units
+                const float4 v3 = v[3];
+                const float2 se = __fmul2_rn(make_float2(v3.x, v3.y), make_float2(ex2_approx(ql.x), ex2_approx(ql.y)));
+                const float2 al = make_float2(q.x <= v2.z ? fminf(0.99f, se.x) : 0.0f,   // alpha >= 1/255
+                                              q.y <= v2.w ? fminf(0.99f, se.y) : 0.0f);  // (R15, R16)
+                const float2 om = __fadd2_rn(f2(1.0f), make_float2(-al.x, -al.y));
+                const float T1 = T * om.x, T2 = T1 * om.y;
+                const float4 v4 = v[4];
+                if (T2 < 1e-4f) {  // R16: a Gaussian of the pair terminates the pixel, before blending
+                    if (T1 >= 1e-4f) {  // the even one still blends
+                        const float w = al.x * T;
+                        C0 = fmaf(v3.z, w, C0);
+                        C1 = fmaf(v4.x, w, C1);
+                        C2 = fmaf(v4.z, w, C2);
+                        T = T1;
+                        if (NC) last = al.x > 0.0f ? base + (uint32_t)k : last;
+                    }
                     done = true;
                     break;
                 }
-                const float w = alpha * T;
-                C0 = fmaf(cl.x, w, C0);
-                C1 = fmaf(cl.y, w, C1);
-                C2 = fmaf(cl.z, w, C2);
-                T = Tn;
-                if (NC) last = contrib ? base + (uint32_t)k : last;
+                const float2 w = __fmul2_rn(al, make_float2(T, T1));
+                C0 = fmaf(v3.w, w.y, fmaf(v3.z, w.x, C0));
+                C1 = fmaf(v4.y, w.y, fmaf(v4.x, w.x, C1));
+                C2 = fmaf(v4.w, w.y, fmaf(v4.z, w.x, C2));
+                T = T2;
+                if (NC) last = al.y > 0.0f ? base + (uint32_t)(k + 1) : (al.x > 0.0f ? base + (uint32_t)k : last);
             }
             st.T[pp] = T;
             st.C0[pp] = C0;
             st.C1[pp] = C1;
             st.C2[pp] = C2;
             if (NC) st.last[pp] = last;
-            st.done[pp] = done ? 1 : 0;
+            my_pp = (uint32_t)pp;
+            my_act = !done;
         }
+        bal = __ballot_sync(0xffffffffu, my_act);
+        if ((tid & 31) == 0) s_warp[tid >> 5] = __popc(bal);
     }
+    cp_async_wait<0>();
     __syncthreads();
     if (inside) {
-        const int p0 = threadIdx.x;
-        const float T = st.T[p0];
+        const float T = st.T[tid];
         const size_t p = (size_t)mpy * W + mpx, plane = (size_t)W * H;
-        out_rgb[p] = fmaf(T, bg0, st.C0[p0]);
-        out_rgb[plane + p] = fmaf(T, bg1, st.C1[p0]);
-        out_rgb[2 * plane + p] = fmaf(T, bg2, st.C2[p0]);
+        out_rgb[p] = fmaf(T, bg0, st.C0[tid]);
+        out_rgb[plane + p] = fmaf(T, bg1, st.C1[tid]);
+        out_rgb[2 * plane + p] = fmaf(T, bg2, st.C2[tid]);
         if (out_T) out_T[p] = T;
-        if (NC) out_nc[p] = st.last[p0];
+        if (NC) out_nc[p] = st.last[tid];
     }
 }
 

@@ -13,6 +13,10 @@ namespace ss {
 namespace {
 
 constexpr int kWarps = kSortThreads / 32;
+#ifndef SS_SORT_LB
+#define SS_SORT_LB 8
+#endif
+constexpr int kLB = SS_SORT_LB;  // look-back predecessors read per round trip
 
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
@@ -107,7 +111,6 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restric
             } else {
                 *lb = kFlagAgg | tot;
                 // walk back kLB predecessors per round trip (independent loads in flight)
-                constexpr int kLB = 8;
                 int p = (int)bid - 1;
                 for (;;) {
                     uint32_t v[kLB];
