@@ -241,7 +241,7 @@ def run_ours(args):
         rz = Rasterizer(ds, W, H, mode=args.mode, capacity=max(1024, 8 * ds.n))
 
     # sizing + per-view statistics (untimed): pairs per frame, visible counts, render work
-    pairs, nvis, E_pix, E_blend, E_cta, ncol = {}, {}, {}, {}, {}, {}
+    pairs, nvis, E_pix, E_blend, E_cta, ncol, dfr = {}, {}, {}, {}, {}, {}, {}
     for v in my_views:
         rz.ensure_capacity(cams[v])
     cap = rz.capacity
@@ -250,7 +250,7 @@ def run_ours(args):
         rz.render()
         t = rz.totals()
         assert not t["overflow"]
-        pairs[v], nvis[v] = t["pairs"], t["n_visible"]
+        pairs[v], nvis[v], dfr[v] = t["pairs"], t["n_visible"], t["deferred"]
         ncol[v] = int(((rz.records()[:, 8] == 1.0) & (rz.depth_keys() != -1)).sum().item())
         st = rz.render_stats()
         E_pix[v], E_blend[v], E_cta[v] = st["E_pix"], st["E_blend"], st["E_cta"]
@@ -598,6 +598,9 @@ def run_ours(args):
             "frame_latency": latency,
             "pairs_per_s": value * Pm,
             "visible_per_frame": NVm,
+            "preprocess_float64_per_frame": {"mean": mean(dfr), "max": max(dfr[v] for v in timed_views),
+                                             "note": "Gaussians whose float32 tile decisions could not be certified "
+                                                     "(evaluated on the float64 path, k_preprocess64)"},
             "coloured_per_frame": mean(ncol),
             "stages_ms": {s: stage_ms[s] for s in stages},
             "host_enqueue_ms_per_frame": host_ms,

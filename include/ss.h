@@ -10,6 +10,22 @@
  *   ss_render      per-tile front-to-back blending     Sec. 3.2.3, Eqs. 5-7
  *   ss_prune_score efficient pruning score, +=         Sec. 4.2.1, Eqs. 20-21
  *
+ * Mapping onto SURVEY.md §8(b)'s proposed signatures (same five calls, same paper steps; one
+ * deviation, stated here and in DESIGN.md §1):
+ *   - ss_preprocess: as proposed (a1 + a2's counts; P, the total, stays on the device).
+ *   - ss_bin + ss_sort: the proposal materialises the paper's unsorted 64-bit keys / values
+ *     (ss_bin, with capacity + overflow flag) and sorts them in place (ss_sort).  Here the
+ *     visible Gaussians are depth-sorted once and the per-tile lists are a stable two-level
+ *     partition of that order, so no unsorted key array ever exists: every pair
+ *     is written once, at its sorted position (sorted_value), and the key is implied by its
+ *     tile (ranges) and depth (depth_key).  The result equals the paper's stable sort of the
+ *     keys emitted in Gaussian-index order; ss_sorted_keys materialises that
+ *     64-bit key array on demand.  ss_bin ends with the tile ranges (a5) because the
+ *     per-tile counts are known before the pairs are written; capacity and the overflow flag
+ *     live in the frame workspace (ss_frame.capacity, ss_layout.overflow / overflow_count).
+ *   - ss_render, ss_prune_score: as proposed; the intermediates are taken from the frame.
+ *   - ss_workspace_size(which, ...): present, over the two workspace kinds (frame, prune step).
+ *
  * Beyond the forward path: the prune step (ss_prune_select,
  * ss_compact_scene; Sec. 4.2), the backward (ss_render_backward, ss_preprocess_backward[_assign];
  * P:404) and the optimisation step of pruning-in-the-loop training (ss_l1_loss_grad,
@@ -142,12 +158,23 @@ typedef struct {
     size_t overflow_count;/* uint32 [1]   sticky: frames with P > capacity since the caller last
                                           zeroed it (libss only increments it; zero it when the
                                           workspace is allocated)                               */
+    size_t pre_deferred;  /* uint32 [1]   Gaussians ss_preprocess evaluated on its float64 path
+                                          (SnugBox / AccuTile: those whose float32 tile decisions
+                                          could not be certified; 3-sigma: all)                 */
     size_t scratch;       /* internal                                                         */
     size_t total_bytes;
     int32_t tiles_x, tiles_y, n_tiles, tile_bits;
 } ss_layout;
 
 SS_API size_t ss_frame_workspace_size(int32_t n, uint32_t capacity, int32_t width, int32_t height);
+
+/* Workspace sizes by kind: SS_WS_FRAME = ss_frame_workspace_size(n, capacity,
+ * width, height); SS_WS_PRUNE = ss_prune_workspace_size(n) (capacity, width, height ignored).
+ * *bytes (host) receives the size; SS_ERR_INVALID_ARG for an unknown kind, n < 0, a null
+ * `bytes`, or (frame) width / height <= 0. */
+typedef enum { SS_WS_FRAME = 0, SS_WS_PRUNE = 1 } ss_workspace_kind;
+SS_API ss_status ss_workspace_size(int which, int32_t n, uint32_t capacity, int32_t width, int32_t height,
+                                   size_t *bytes /*host*/);
 SS_API ss_status ss_frame_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height, ss_layout *out /*host*/);
 
 /* a1 -- preprocess (Sec. 3.2.1; count mode of SnugBox/AccuTile).

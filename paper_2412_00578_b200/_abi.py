@@ -12,7 +12,7 @@ LIB_PATH = os.path.join(HERE, "libss.so")
 SS_OK, SS_ERR_INVALID_ARG, SS_ERR_CAPACITY, SS_ERR_CUDA, SS_ERR_UNSUPPORTED = range(5)
 MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}
 
-EXPORTS = ["ss_frame_workspace_size", "ss_frame_layout", "ss_preprocess", "ss_bin", "ss_sort", "ss_sorted_keys",
+EXPORTS = ["ss_frame_workspace_size", "ss_workspace_size", "ss_frame_layout", "ss_preprocess", "ss_bin", "ss_sort", "ss_sorted_keys",
            "ss_render", "ss_render_stats", "ss_finalize_colours", "ss_prune_score", "ss_render_frame",
            "ss_prune_workspace_size", "ss_prune_count", "ss_prune_select", "ss_compact_scene",
            "ss_render_backward", "ss_preprocess_backward", "ss_l1_loss_grad", "ss_adam_init", "ss_adam_step",
@@ -37,7 +37,7 @@ class SsFrame(C.Structure):
 
 class SsLayout(C.Structure):
     _fields_ = [(k, C.c_size_t) for k in ("rec", "erec", "depth_key", "order", "sorted_value", "tile_count", "ranges", "n_visible", "total_pairs",
-                                          "overflow", "overflow_count", "scratch", "total_bytes")] + \
+                                          "overflow", "overflow_count", "pre_deferred", "scratch", "total_bytes")] + \
                [(k, C.c_int32) for k in ("tiles_x", "tiles_y", "n_tiles", "tile_bits")]
 
 
@@ -64,6 +64,7 @@ def lib() -> C.CDLL:
         sig = {
             "ss_frame_workspace_size": (C.c_size_t, [C.c_int32, C.c_uint32, C.c_int32, C.c_int32]),
             "ss_frame_layout": (st, [C.c_int32, C.c_uint32, C.c_int32, C.c_int32, P(SsLayout)]),
+            "ss_workspace_size": (st, [st, C.c_int32, C.c_uint32, C.c_int32, C.c_int32, P(C.c_size_t)]),
             "ss_preprocess": (st, [P(SsScene), P(SsCamera), st, P(SsFrame), vp]),
             "ss_bin": (st, [P(SsCamera), st, P(SsFrame), vp]),
             "ss_sort": (st, [P(SsFrame), vp]),

@@ -69,7 +69,10 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     P.n_visible = take(4);
     P.total_pairs = take(4);
     L->hist_depth = take(4 * 256 * kDepthPasses);
+    L->pre_queue_n = take(4);
     L->zero_pre_end = off;
+    L->pre_queue = L->dkA;
+    P.pre_deferred = L->pre_queue_n;
     L->zero_bin = off;  // written by ss_bin
     L->counters = take(4 * 16);
     L->lb_depth = take(4 * 256 * (size_t)L->nblk_depth * kDepthPasses);
@@ -140,6 +143,21 @@ size_t ss_frame_workspace_size(int32_t n, uint32_t capacity, int32_t width, int3
     Layout L;
     if (!compute_layout(n, capacity, width, height, &L)) return 0;
     return L.pub.total_bytes;
+}
+
+ss_status ss_workspace_size(int which, int32_t n, uint32_t capacity, int32_t width, int32_t height, size_t *bytes) {
+    if (!bytes || n < 0) return SS_ERR_INVALID_ARG;
+    if (which == SS_WS_FRAME) {
+        Layout L;
+        if (!compute_layout(n, capacity, width, height, &L)) return SS_ERR_INVALID_ARG;
+        *bytes = L.pub.total_bytes;
+        return SS_OK;
+    }
+    if (which == SS_WS_PRUNE) {
+        *bytes = prune_workspace_bytes(n);
+        return SS_OK;
+    }
+    return SS_ERR_INVALID_ARG;
 }
 
 ss_status ss_frame_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height, ss_layout *out) {

@@ -17,6 +17,16 @@ constexpr int kWarps = kSortThreads / 32;
 #define SS_SORT_LB 8
 #endif
 constexpr int kLB = SS_SORT_LB;  // look-back predecessors read per round trip
+#ifndef SS_SORT_SLEEP
+#define SS_SORT_SLEEP 0
+#endif
+constexpr int kLBSleepNs = SS_SORT_SLEEP;
+#ifndef SS_SORT_GRID
+#define SS_SORT_GRID 4  // persistent onesweep CTAs per SM
+#endif
+#ifndef SS_SORT_MATCH
+#define SS_SORT_MATCH 0
+#endif  // back-off when no predecessor has published yet
 
 template <typename K>
 __device__ __forceinline__ uint32_t digit_of(K key, int shift) {
@@ -77,19 +87,34 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restric
             const size_t idx = wbase + (size_t)j * 32;
             key[j] = idx < n ? (uint32_t)keys_in[idx] : 0xFFFFFFFFu;
         }
-        // 2. warp-level stable ranking (8 ballots per item = match on the digit)
+        // 2. warp-level stable ranking: the lanes holding the same digit (SS_SORT_MATCH: one
+        //    match.any; else 8 ballots on the digit bits), then the warp's running count of that
+        //    digit by one shared-memory atomic of the leader lane (fetch-and-add: no dependent
+        //    load -> store chain per item); __syncwarp orders item j's atomics before item j+1's,
+        //    so item j+1 sees the counts of items <= j (a stable rank).
 #pragma unroll
         for (int j = 0; j < kSortItems; ++j) {
             const size_t idx = wbase + (size_t)j * 32;
             const bool valid = idx < n && (!FILTER || key[j] != kNoTiles);
             const uint32_t d = digit_of(key[j], shift);
-            const uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 256u + (uint32_t)lane);
+#if SS_SORT_MATCH
+            const uint32_t peers = valid ? __match_any_sync(0xffffffffu, valid ? d : 256u + (uint32_t)lane) : 0u;
+#else
+            uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int bit = 0; bit < 8; ++bit) {
+                const bool v = (d >> bit) & 1u;
+                const uint32_t m = __ballot_sync(0xffffffffu, v);
+                peers &= v ? m : ~m;
+            }
+            peers = valid ? peers : 0u;
+#endif
             const uint32_t lt = __popc(peers & lanemask_lt);
+            const int leader = peers ? __ffs(peers) - 1 : lane;
             uint32_t prev = 0;
-            if (valid) prev = s_whist[warp][d];
-            __syncwarp();
-            if (valid && lt == 0) s_whist[warp][d] = prev + __popc(peers);
-            __syncwarp();
+            if (valid && lt == 0) prev = atomicAdd(&s_whist[warp][d], (uint32_t)__popc(peers));
+            __syncwarp();  // orders item j's atomics before item j+1's (memory ordering within the warp)
+            prev = __shfl_sync(0xffffffffu, prev, leader);
             const uint32_t r = valid ? prev + lt : 0xFFFFu;
             if (j & 1) rank2[j >> 1] |= r << 16;
             else rank2[j >> 1] = r;
@@ -139,6 +164,7 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restric
                     prefix += add;
                     p -= used;
                     if (inc) break;
+                    if (kLBSleepNs > 0 && used == 0) __nanosleep(kLBSleepNs);  // free the issue slots
                 }
                 *lb = kFlagInc | (prefix + tot);
             }
@@ -185,7 +211,7 @@ __global__ void k_sorted_keys(const uint2 *__restrict__ ranges, const uint32_t *
 
 int sort_grid(uint32_t nblk) {
     const int sms = sm_count();
-    const uint32_t cap = (uint32_t)sms * 4;
+    const uint32_t cap = (uint32_t)sms * SS_SORT_GRID;
     return (int)(nblk < cap ? (nblk ? nblk : 1) : cap);
 }
 

@@ -139,7 +139,8 @@ class Rasterizer:
         nv = int(self._view(self.layout.n_visible, 1, torch.int32).item())
         P = int(self._view(self.layout.total_pairs, 1, torch.int32).item()) & 0xFFFFFFFF
         ov = int(self._view(self.layout.overflow, 1, torch.int32).item())
-        return {"n_visible": nv, "pairs": P, "overflow": ov}
+        dfr = int(self._view(self.layout.pre_deferred, 1, torch.int32).item())
+        return {"n_visible": nv, "pairs": P, "overflow": ov, "deferred": dfr}
 
     def overflow_count(self) -> int:
         """Frames of this workspace whose pairs exceeded the capacity since the last

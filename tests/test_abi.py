@@ -37,6 +37,15 @@ def test_layout_and_workspace(lib):
     L2 = _abi.layout(10, 100, 1297, 840)
     assert (L2.tiles_x, L2.tiles_y, L2.tile_bits) == (82, 53, 13)
     assert _abi.workspace_size(-1, 10, 10, 10) == 0
+    # §8(b)'s ss_workspace_size(which, ...): the frame and prune-step workspaces
+    b = C.c_size_t(0)
+    assert lib.ss_workspace_size(0, 1000, 4096, 256, 256, C.byref(b)) == _abi.SS_OK
+    assert b.value == L.total_bytes
+    assert lib.ss_workspace_size(1, 1000, 0, 0, 0, C.byref(b)) == _abi.SS_OK
+    assert b.value == lib.ss_prune_workspace_size(1000)
+    assert lib.ss_workspace_size(2, 1000, 0, 0, 0, C.byref(b)) == _abi.SS_ERR_INVALID_ARG
+    assert lib.ss_workspace_size(0, 1000, 0, 0, 16, C.byref(b)) == _abi.SS_ERR_INVALID_ARG
+    assert lib.ss_workspace_size(0, -1, 0, 16, 16, C.byref(b)) == _abi.SS_ERR_INVALID_ARG
 
 
 def test_invalid_arguments_rejected_before_launch(lib):
