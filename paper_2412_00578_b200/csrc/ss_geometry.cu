@@ -142,10 +142,14 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess64(int n,
     const int stx = (cam.tiles_x + kSuper - 1) / kSuper;
     const int lane = threadIdx.x & 31;
     const int n_items = queue ? (int)*queue_n : n;
-    // warp-uniform grid-stride loop (the tall-Gaussian phase below is warp-collective)
-    for (int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n_items; i0 += gridDim.x * blockDim.x) {
-        const bool valid = i0 + lane < n_items;
-        const int i = queue ? (valid ? (int)queue[i0 + lane] : 0) : i0 + lane;
+    // warp-uniform grid-stride loop (the tall-Gaussian phase below is warp-collective).  Over all
+    // Gaussians: 32 per warp step.  Over the queue (a few hundred, many of them tall): one per
+    // warp step, so that the queued work spreads over as many warps as possible.
+    const int per_step = queue ? 1 : 32;
+    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int i0 = gwarp * per_step; i0 < n_items; i0 += nwarps * per_step) {
+        const bool valid = queue ? (lane == 0) : (i0 + lane < n_items);
+        const int i = queue ? (valid ? (int)queue[i0] : 0) : i0 + lane;
         uint32_t count = 0;
         const float4 mo = valid ? mean_opac[i] : make_float4(0.f, 0.f, -1.f, 0.f);
         const float4 q4 = valid ? rot[i] : make_float4(1.f, 0.f, 0.f, 0.f);  // issued with the mean
@@ -384,6 +388,8 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
                                 if (w.s1 - w.s0 > kLaneRows) {
                                     tall = true;  // the warp-cooperative sweep below
                                 } else {
+                                    // line spans into the emission record (the binning derives
+                                    // the entries from them); here only the entry count
                                     EntryCount ec;
                                     cnt_init(ec);
                                     const bool ok = accutile_count32(w, count, [&](int r, int lo, int hi) {
@@ -562,7 +568,7 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
                    at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs),
                    queue, queue_n, csrc, at<ColorSrc>(ws, L.color_src));
     // the deferred Gaussians on the float64 path (a few CTAs; the queue length is on the device)
-    launch_pdl(k_preprocess64, sms, kPreThreads, 0, st, SS_PRE64_ARGS(queue, queue_n));
+    launch_pdl(k_preprocess64, sms * kPreBlocks, kPreThreads, 0, st, SS_PRE64_ARGS(queue, queue_n));
     if (e != cudaSuccess) return e;
 #undef SS_PRE64_ARGS
     return cudaGetLastError();
