@@ -145,7 +145,7 @@ __device__ __forceinline__ void span_entries(uint2 *__restrict__ stg, uint32_t g
     acc_init(acc, (info & kInfoCols) != 0, stx);
     uint32_t e = eo;
     auto out = [&](uint32_t st, uint32_t mask) { put_entry(stg, e++, st, g, mask); };
-#pragma unroll
+#pragma unroll 1
     for (int q = 0; q < 6; ++q)
         if ((uint32_t)q < ns)
             acc_feed(acc, (int)(v[q] >> 18), (int)(v[q] & 0x1FFu), (int)((v[q] >> 9) & 0x1FFu), out);
@@ -235,20 +235,29 @@ __global__ void __launch_bounds__(256) k_entries(const uint32_t *__restrict__ n_
     if (*overflow) return;
     const uint32_t nv = *n_visible;
     const int lane = threadIdx.x & 31;
-    for (uint32_t k0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); k0 < nv; k0 += gridDim.x * blockDim.x) {
+    // the order / offset of the next grid-stride step are loaded one step ahead, and the whole
+    // 32 B record (one sector) with one pair of independent loads: one dependent round trip
+    // (order -> record) per Gaussian, overlapped with the previous Gaussian's work
+    const uint32_t stride = gridDim.x * blockDim.x;
+    uint32_t k0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31u);
+    uint32_t g_n = 0, eo_n = 0;
+    if (k0 + lane < nv) {
+        g_n = order[k0 + lane];
+        eo_n = eoff[k0 + lane];
+    }
+    for (; k0 < nv; k0 += stride) {
         const uint32_t k = k0 + lane;
         const bool act = k < nv;
-        uint32_t g = 0, eo = 0;
+        const uint32_t g = g_n, eo = eo_n;
         uint4 e0 = make_uint4(0u, 0u, 0u, 0u), e1 = e0;
         if (act) {
-            g = order[k];
-            eo = eoff[k];
-            const uint4 *er = erec + 2 * (size_t)g;  // 32 B emission record: the words in use
+            const uint4 *er = erec + 2 * (size_t)g;  // 32 B emission record
             e0 = er[0];
-            const uint32_t info = e0.y;
-            const uint32_t words = (info & kInfoSpanInline) ? (info & 0xFFu)
-                                   : (info & kInfoEntInline) ? (info >> kInfoEntShift) : 0u;
-            if (words > 2) e1 = er[1];
+            e1 = er[1];
+        }
+        if (k + stride < nv) {
+            g_n = order[k + stride];
+            eo_n = eoff[k + stride];
         }
         const bool spn = (e0.y & kInfoSpanInline) != 0, ent = (e0.y & kInfoEntInline) != 0;
         if (act && spn) span_entries(stg, g, eo, e0.y, e0, e1, stx);
