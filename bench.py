@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--prune-ratio", type=float, default=0.0,
                     help="pruned-model regime: score all views (a7 + all_reduce), prune this fraction, bench the rest")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graphs", action="store_true", help="enqueue every frame's kernels instead of one CUDA graph")
+    ap.add_argument("--no-pruned", action="store_true", help="skip the pruned-regime (config 5) measurement")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-score", action="store_true")
     ap.add_argument("--no-backward", action="store_true")
@@ -288,8 +290,18 @@ def run_ours(args):
             e[4].record(stream)
 
     pipe = FramePipeline(ds, W, H, mode=args.mode, n_streams=args.streams, capacity=rz.capacity)
+    graphs = not args.no_graphs
+    graph_info = None
+    if graphs:
+        # one CUDA graph per (view, workspace): the frame's ~20 launches become one graph launch
+        pipe.render_views([cstructs[v] for v in my_views[:args.streams]])   # first-call setup outside capture
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        n_graphs = pipe.capture([cstructs[v] for v in my_views])
+        graph_info = {"graphs": n_graphs, "capture_s": time.perf_counter() - g0,
+                      "note": "per (view, workspace): ss_render_frame captured once, replayed every step"}
     for j in range(args.warmup):
-        pipe.render_views([cstructs[v] for v in seq[j * V:(j + 1) * V]])
+        pipe.render_views([cstructs[v] for v in seq[j * V:(j + 1) * V]], graphs=graphs)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     if not args.ncu:
@@ -309,7 +321,7 @@ def run_ours(args):
     for k in range(args.steps):
         flush.zero_()
         t_ev[k][0].record(stream)
-        pipe.render_views([cstructs[v] for v in timed_views[k * V:(k + 1) * V]])
+        pipe.render_views([cstructs[v] for v in timed_views[k * V:(k + 1) * V]], graphs=graphs)
         t_ev[k][1].record(stream)
     host_ms = (time.perf_counter() - h0) * 1e3 / n_timed
     torch.cuda.synchronize()
@@ -552,19 +564,61 @@ def run_ours(args):
         n_e = min(len(my_views), V)
         host = [torch.empty((3, H, W), dtype=torch.float32).pin_memory() for _ in range(n_e)]
         vs = [cams[v] for v in my_views[:n_e]]
-        render_views_to_host(pipe, vs, host)
+        render_views_to_host(pipe, vs, host, graphs=graphs)
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         reps = max(1, args.steps // 4)
         for _ in range(reps):
-            render_views_to_host(pipe, vs, host)
+            render_views_to_host(pipe, vs, host, graphs=graphs)
         dt = dist.max_over_ranks(time.perf_counter() - t0)
         e2e = {"value": world * reps * n_e / dt, "unit": "frames/s",
                "h2d_bytes_per_step": V * ctypes.sizeof(SsCamera), "d2h_bytes_per_step": V * 3 * H * W * 4,
-               "note": "scene resident in HBM; per frame the camera goes host->device as kernel arguments and "
-                       "the float32 image device->host into pinned memory, copied on the frame's own stream "
+               "note": "scene resident in HBM; per frame the camera (host struct) selects the frame's launch (" +
+                       ("its pre-captured CUDA graph" if graphs else "kernel arguments") + ") and the float32 "
+                       "image goes device->host into pinned memory, copied on the frame's own stream "
                        f"({args.streams} frames in flight: copies overlap the other streams' kernels)"}
+
+    # ---- pruned-model regime (BASELINE config 5): U~ over every view (this rank's shard, then the
+    # all_reduce), the prune step removing 90%, then the same timed loop on the pruned scene
+    pruned_info = None
+    if not args.no_pruned and not args.ncu and prune_info is None:
+        ratio = 0.9
+        t0 = time.perf_counter()
+        score_all = torch.zeros(ds.n, dtype=torch.float64, device=dev)
+        pipe.score_views([cstructs[v] for v in my_views], score_all)
+        torch.cuda.synchronize()
+        pipe.check_overflow()
+        dist.allreduce_scores(score_all)
+        pds, _ = prune(ds, score_all, ratio)
+        del score_all
+        ppipe = FramePipeline(pds, W, H, mode=args.mode, n_streams=args.streams)
+        pP = ppipe.ensure_capacity([cstructs[v] for v in my_views], headroom=1.02)
+        if graphs:
+            ppipe.render_views([cstructs[v] for v in my_views[:args.streams]])
+            ppipe.capture([cstructs[v] for v in my_views])
+        setup_s = time.perf_counter() - t0
+        for j in range(args.warmup):
+            ppipe.render_views([cstructs[v] for v in seq[j * V:(j + 1) * V]], graphs=graphs)
+        dist.barrier()
+        torch.cuda.synchronize()
+        pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for k in range(args.steps):
+            flush.zero_()
+            pev[k][0].record(stream)
+            ppipe.render_views([cstructs[v] for v in timed_views[k * V:(k + 1) * V]], graphs=graphs)
+            pev[k][1].record(stream)
+        torch.cuda.synchronize()
+        assert ppipe.overflow_count() == 0
+        pms = dist.max_over_ranks(sum(a.elapsed_time(b) for a, b in pev))
+        pval = world * n_timed / (pms / 1e3)
+        pruned_info = {"value": pval, "unit": "frames/s", "ratio": ratio, "n_gaussians": pds.n,
+                       "ms_per_frame": pms / n_timed, "max_pairs_per_frame": pP, "speedup_vs_unpruned": pval / value,
+                       "setup_s": setup_s,
+                       "note": "BASELINE config 5 on 1 scene: U~ over every view (sharded, all_reduce), prune step "
+                               "(lowest 90% removed, ties by index), no fine-tuning; the same timed loop, L2 flushed "
+                               "between steps"}
+        del ppipe, pds
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
@@ -592,6 +646,8 @@ def run_ours(args):
                        "process_group": dist.backend() or "none (1 rank)",
                        "gpus_visible": torch.cuda.device_count(), "ranks_per_gpu": ranks_per_gpu,
                        "frames_in_flight": args.streams,
+                       "launch": "one CUDA graph per frame (captured per view and workspace)" if graphs
+                                 else "one ss_render_frame call per frame",
                        "l2": "flushed between steps (256 MB written outside the timed regions); scene %.0f MB, "
                              "per-frame records %.0f MB" % (ds.n * 240 / 1e6, NVm * 48 / 1e6)},
             "pairs_per_frame": {"mean": Pm, "min": min(pairs.values()), "max": max(pairs.values())},
@@ -604,6 +660,7 @@ def run_ours(args):
             "coloured_per_frame": mean(ncol),
             "stages_ms": {s: stage_ms[s] for s in stages},
             "host_enqueue_ms_per_frame": host_ms,
+            "graphs": graph_info,
             "stages": stage_info,
             "render_work": {"E_pix": mean(E_pix), "E_blend": mean(E_blend), "E_cta": mean(E_cta),
                             "pixels": W * H},
@@ -617,6 +674,7 @@ def run_ours(args):
             "prune_score": score_info,
             "backward": bw_info,
             "train": train_info,
+            "pruned": pruned_info,
             "cpu_baseline": cpu,
             "paper_context": {"gpu": "RTX A5000 (PAPER.md P:447)", "accutile_fps_avg_scene": 267,
                               "speedups": {"snugbox": 1.82, "accutile": 1.99, "overall": 6.71}},

@@ -287,6 +287,44 @@ class FramePipeline:
         dev = self.rz[0].device
         self.streams = [torch.cuda.Stream(device=dev) for _ in range(self.n_streams)]
         self.outs = [torch.empty((3, height, width), dtype=torch.float32, device=dev) for _ in range(self.n_streams)]
+        self._graphs = {}   # (workspace, camera bytes, bg) -> CUDA graph of that frame's a1-a6
+
+    # ---------------------------------------------------------------- CUDA graphs
+    def _graph_key(self, k: int, c: SsCamera, bg) -> tuple:
+        return (k, bytes(c), tuple(float(v) for v in bg))
+
+    def capture(self, cams, bg=(0.0, 0.0, 0.0)) -> int:
+        """Capture, for every camera and every workspace, the frame's whole launch sequence
+        (ss_render_frame: 2 memsets + the a1-a6 kernels with their programmatic dependent
+        launches) into a CUDA graph, so that render_views(..., graphs=True) enqueues a frame
+        with one graph launch instead of ~20 kernel launches (the host enqueue otherwise
+        approaches the GPU time per frame).  The graphs bake in the camera, the workspace and
+        its output buffer; re-capture after ensure_capacity() reallocates.  Returns the number
+        of graphs captured (synchronises)."""
+        bgv = (C.c_float * 3)(*[float(v) for v in bg])
+        mode = MODES[self.rz[0].mode]
+        fn = lib().ss_render_frame
+        n = 0
+        for cam in cams:
+            c = camera_struct(cam)
+            for k, (rz, st) in enumerate(zip(self.rz, self.streams)):
+                key = self._graph_key(k, c, bg)
+                if key in self._graphs:
+                    continue
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.stream(st):
+                    g.capture_begin()
+                    status = fn(C.byref(rz._scene_struct), C.byref(c), mode, C.byref(rz.frame), bgv,
+                                C.c_void_p(self.outs[k].data_ptr()), None, None, C.c_void_p(int(st.cuda_stream)))
+                    g.capture_end()
+                check(status, "ss_render_frame (capture)")
+                self._graphs[key] = g
+                n += 1
+        torch.cuda.synchronize()
+        return n
+
+    def drop_graphs(self) -> None:
+        self._graphs.clear()
 
     def ensure_capacity(self, cams, headroom: float = 1.02) -> int:
         """Size every workspace for the largest pair count over `cams` (synchronises)."""
@@ -295,6 +333,7 @@ class FramePipeline:
         for r in self.rz:
             if r.capacity != cap:
                 r._alloc(cap)
+                self._graphs.clear()   # the graphs point at the old workspaces
         self.clear_overflow()
         return P
 
@@ -317,7 +356,7 @@ class FramePipeline:
             raise _abi.SsError(f"{k} frame(s) exceeded the pair capacity {self.rz[0].capacity}; "
                                f"call ensure_capacity() for these cameras and re-run them")
 
-    def render_views(self, cams, bg=(0.0, 0.0, 0.0), on_frame=None, pre_events=None) -> None:
+    def render_views(self, cams, bg=(0.0, 0.0, 0.0), on_frame=None, pre_events=None, graphs: bool = False) -> None:
         """Render every camera (a1-a6).  on_frame(j, image, stream) is called right after
         frame j is enqueued, on its stream (e.g. to enqueue a device->host copy); image is
         that stream's output buffer, reused by the stream's next frame.  pre_events[j]
@@ -326,6 +365,22 @@ class FramePipeline:
         cur = torch.cuda.current_stream()
         for st in self.streams:
             st.wait_stream(cur)
+        if graphs:
+            # one graph launch per frame on its workspace's stream (capture() must have seen
+            # every (camera, workspace) pair); on_frame runs after the frame's launch
+            for j, cam in enumerate(cams):
+                k = j % self.n_streams
+                c = camera_struct(cam)
+                g = self._graphs.get(self._graph_key(k, c, bg))
+                if g is None:
+                    raise _abi.SsError("render_views(graphs=True): frame not captured; call capture(cams) first")
+                with torch.cuda.stream(self.streams[k]):
+                    g.replay()
+                    if on_frame is not None:
+                        on_frame(j, self.outs[k], self.streams[k])
+            for st in self.streams:
+                cur.wait_stream(st)
+            return
         if pre_events is None and on_frame is None:
             # the plain path: one C-ABI call per frame (ss_render_frame = a1-a6), no per-frame
             # Python stream contexts -- the host enqueues a frame in a fraction of its GPU time
@@ -382,7 +437,7 @@ class FramePipeline:
         return score
 
 
-def render_views_to_host(pipe: "FramePipeline", cams, host_out: list, bg=(0.0, 0.0, 0.0)) -> None:
+def render_views_to_host(pipe: "FramePipeline", cams, host_out: list, bg=(0.0, 0.0, 0.0), graphs: bool = False) -> None:
     """End-to-end public call: render each camera and land its image in pinned host memory.
 
     Frames run on the pipeline's streams; frame j's device->host copy is enqueued on its own
@@ -392,7 +447,7 @@ def render_views_to_host(pipe: "FramePipeline", cams, host_out: list, bg=(0.0, 0
     def copy(j, img, st):
         host_out[j].copy_(img, non_blocking=True)
     cs = [camera_struct(c) for c in cams]
-    pipe.render_views(cs, bg, on_frame=copy)
+    pipe.render_views(cs, bg, on_frame=copy, graphs=graphs)
     torch.cuda.current_stream().synchronize()
     if pipe.overflow_count():   # a view needed more pairs than the workspaces hold: grow, redo
         pipe.clear_overflow()

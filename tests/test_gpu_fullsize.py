@@ -1,8 +1,8 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
 
 Every frame here runs through the bench's exact timed path: a FramePipeline of 4 workspaces on
-4 streams, workspaces sized as the bench sizes them (max P + 2% + 4096), each frame enqueued by
-one ss_render_frame call (a1-a6).  The oracle (forked worker processes, one view each) then
+4 streams, workspaces sized as the bench sizes them (max P + 2% + 4096), each frame enqueued as
+one CUDA graph replay of its captured ss_render_frame call (a1-a6).  The oracle (forked worker processes, one view each) then
 checks, per view and with nothing sampled:
 
 * every Gaussian's tile count, the full sorted key and value lists and the tile ranges,
@@ -58,7 +58,8 @@ def _check_views(name, views, mode, bg=(0.0, 0.0, 0.0), score=False):
     _W[name] = (scene, cams)
     ds, pipe = _pipeline(scene, cams, views, mode)
     assert len(views) <= pipe.n_streams  # one view per workspace: every intermediate stays inspectable
-    pipe.render_views([cams[v] for v in views], bg)
+    pipe.capture([cams[v] for v in views], bg)                 # bench.py's timed path: one CUDA graph per
+    pipe.render_views([cams[v] for v in views], bg, graphs=True)  # (view, workspace)
     torch.cuda.synchronize()
     refs = _oracle_views(name, views, mode, bg, score)
     out = {"views": len(views), "values_checked": 0}

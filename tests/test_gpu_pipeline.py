@@ -40,6 +40,19 @@ def test_pipeline_images_equal_single_stream(n_streams):
     render_views_to_host(pipe, cams, host, (0.1, 0.0, 0.2))
     for j in range(len(cams)):
         assert np.array_equal(host[j].numpy(), ref[j]), j
+    # CUDA graphs (one per view and workspace, bench.py's timed path): replays twice give the
+    # same images, through the callback and the end-to-end host path
+    assert pipe.capture(cams, (0.1, 0.0, 0.2)) == len(cams) * n_streams
+    for _ in range(2):
+        got = [None] * len(cams)
+        pipe.render_views([camera_struct(c) for c in cams], (0.1, 0.0, 0.2), on_frame=keep, graphs=True)
+        torch.cuda.synchronize()
+        for j in range(len(cams)):
+            assert np.array_equal(got[j].cpu().numpy(), ref[j]), j
+    host = [torch.empty((3, 136, 200), dtype=torch.float32).pin_memory() for _ in cams]
+    render_views_to_host(pipe, cams, host, (0.1, 0.0, 0.2), graphs=True)
+    for j in range(len(cams)):
+        assert np.array_equal(host[j].numpy(), ref[j]), j
 
 
 def test_pipeline_score_views_equal_single_stream():
