@@ -393,12 +393,15 @@ def run_ours(args):
         tj = json.load(open(tpath))
         tsrc = tj.get("source")
         for k, v in tj.get("kernels", {}).items():
+            # ss_preprocess = k_preprocess32 (+ k_preprocess64 over its deferred queue): summed
             for kn in ("k_preprocess", "k_render<"):
                 if k.startswith(kn):
-                    traffic[kn.rstrip("<")] = v["dram_bytes"]
+                    traffic[kn.rstrip("<")] = traffic.get(kn.rstrip("<"), 0.0) + v["dram_bytes"]
     pre = stage_info["preprocess"]
     kern = {
-        "k_preprocess": {"bound": "hbm", "launch_ms": pre_iso_ms, "achieved": pre["achieved"], "peak": hbm_peak,
+        "k_preprocess": {"bound": "hbm", "launch_ms": pre_iso_ms,
+                         "launches": "k_preprocess32 (float32-certified tile geometry) + k_preprocess64 (the "
+                                     "float64 path over the deferred queue, a few hundred Gaussians)", "achieved": pre["achieved"], "peak": hbm_peak,
                          "unit": "GB/s", "frac": pre["frac"], "algorithmic_bytes": pre["bytes"],
                          "traffic": traffic.get("k_preprocess"), "peak_source": hbm_src,
                          "unit_work": "16 B per Gaussian + 4 B depth key + per visible Gaussian 32 B scale/rot "

@@ -24,7 +24,7 @@ launches)
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --ncu --no-backward --steps 1 --warmup 1 --views-per-step 2 > /dev/null 2>&1; echo ncu_launches=$?
   python profiles/summarize.py launches gpurun_out/${TAG}_launches.csv ;;
 chain)
-  timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -o gpurun_out/${TAG}_chain python scripts/profile_frame.py > gpurun_out/${TAG}_chain.log 2>&1; echo ncu_chain=$?
+  timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -o gpurun_out/${TAG}_chain python scripts/profile_frame.py ${PROF_ARGS} > gpurun_out/${TAG}_chain.log 2>&1; echo ncu_chain=$?
   ncu -i gpurun_out/${TAG}_chain.ncu-rep --page raw --csv > gpurun_out/${TAG}_chain_raw.csv 2>/dev/null
   python profiles/summarize.py full gpurun_out/${TAG}_chain.ncu-rep > gpurun_out/${TAG}_chain.txt; head -3 gpurun_out/${TAG}_chain.txt ;;
 prof)
