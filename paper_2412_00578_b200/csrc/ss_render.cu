@@ -402,7 +402,9 @@ __global__ void __launch_bounds__(256, 6) k_prune_score(const uint2 *__restrict_
             const uint32_t plast = act ? st.last[pp] : 0u;
             const float Tfin = s_Tfin[pp];
             float T = act ? st.T[pp] : 1.0f;
-            float S0 = st.C0[pp], S1 = st.C1[pp], S2 = st.C2[pp];
+            // inactive lanes (pp = 0 placeholder) read nothing: pixel 0's state may be written by
+            // its own lane in this phase
+            float S0 = act ? st.C0[pp] : 0.0f, S1 = act ? st.C1[pp] : 0.0f, S2 = act ? st.C2[pp] : 0.0f;
             for (int k = cnt - 1; k >= 0; --k) {
                 float term = 0.f;
                 if (start - range.x + (uint32_t)k < plast) {
@@ -520,8 +522,10 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
             const float Tfin = s_Tfin[pp];
             float *wpart = s_part + (size_t)warp * kBatch * 9;
             const float dC0 = s_dC[0][pp], dC1 = s_dC[1][pp], dC2 = s_dC[2][pp];
-            float T = st.T[pp];
-            float S0 = st.C0[pp], S1 = st.C1[pp], S2 = st.C2[pp];
+            float T = act ? st.T[pp] : 1.0f;
+            // inactive lanes (pp = 0 placeholder) read nothing: pixel 0's state may be written by
+            // its own lane in this phase
+            float S0 = act ? st.C0[pp] : 0.0f, S1 = act ? st.C1[pp] : 0.0f, S2 = act ? st.C2[pp] : 0.0f;
             for (int k = cnt - 1; k >= 0; --k) {
                 float g[9];
 #pragma unroll

@@ -92,10 +92,11 @@ class Rasterizer:
     def _alloc(self, capacity: int) -> None:
         capacity = int(min(capacity, (1 << 30) - 1))
         nbytes = _abi.workspace_size(self.scene.n, capacity, self.width, self.height)
-        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        # zero-filled once: the sticky overflow counter starts at 0, and the kernels' reads of
+        # record words they never use (a 32 B emission record is read whole) see defined bytes
+        self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.device)
         self.capacity = capacity
         self.layout = _abi.layout(self.scene.n, capacity, self.width, self.height)
-        self.ws[self.layout.overflow_count: self.layout.overflow_count + 4].zero_()   # sticky counter
         self.frame = SsFrame(self.ws.data_ptr(), nbytes, self.scene.n, capacity, self.width, self.height)
         self.n_tiles = self.layout.n_tiles
 

@@ -30,6 +30,10 @@ chain)
 prof)
   timeout 900 ncu --profile-from-start off --set full --clock-control none --import-source on -k regex:"${KREGEX:-k_render}" -o gpurun_out/${TAG}_prof python scripts/profile_frame.py ${PROF_ARGS} > gpurun_out/${TAG}_prof.log 2>&1; echo ncu_prof=$?
   ncu -i gpurun_out/${TAG}_prof.ncu-rep --page raw --csv > gpurun_out/${TAG}_prof_raw.csv 2>/dev/null ;;
+sanitize)
+  for tool in memcheck racecheck synccheck initcheck; do
+    timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python scripts/sanitize_run.py > gpurun_out/${TAG}_sanitize_$tool.txt 2>&1; echo sanitize_$tool=$?; tail -2 gpurun_out/${TAG}_sanitize_$tool.txt
+  done ;;
 full)
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:'k_(preprocess|emit|render|onesweep|tile_finalize|render_backward|preprocess_backward)' -s 40 -c 12 -o gpurun_out/${TAG}_full python bench.py --ncu --steps 1 --warmup 1 --views-per-step 2 > gpurun_out/${TAG}_full.log 2>&1; echo ncu_full=$? ;;
 esac; done
