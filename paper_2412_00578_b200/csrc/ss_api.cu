@@ -62,6 +62,8 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     P.tile_count = take(4 * T);
     L->tile_base = take(4 * T);
     L->color_src = take(64);
+    L->pix_T = take(4 * (size_t)width * (size_t)height);
+    L->pix_last = take(4 * (size_t)width * (size_t)height);
     P.overflow = take(4);
     P.overflow_count = take(4);
     // ---- regions each call clears for itself (so every call is idempotent given its inputs)

@@ -63,6 +63,7 @@ struct Layout {
     size_t l2_BC;                   // uint32 [l2_max_blocks][16] pairs per (block, tile) -> prefix
     size_t tile_base;               // uint32 [n_tiles] first sorted position of each tile
     size_t color_src;               // ColorSrc (64 B): scene mean / SH pointers + camera centre of the frame
+    size_t pix_T, pix_last;         // float / uint32 [W*H]: ss_prune_score's forward (T_final, n_contrib)
     size_t zero_pre, zero_pre_end;  // regions each call clears for itself
     size_t zero_bin, zero_bin_end;
     size_t hist_depth;              // uint32 [4][256]

@@ -107,8 +107,9 @@ struct RawBatch {
     float4 q[3 * kBatch];  // records as gathered: q0, q1, q2 per slot
 };
 // Pair-interleaved (AoSoA) layout: Gaussians 2p and 2p+1 share 20 floats, so that one 128-bit
-// shared load gives two fields of the pair as two f32x2 operands:
-//   [-x0 -x1 -y0 -y1] [a0 a1 2b0 2b1] [c0 c1 t0 t1] [s0 s1 r0 r1] [g0 g1 bl0 bl1]
+// shared load gives two fields of the pair as two f32x2 operands, and the (r, g) of each
+// Gaussian as one f32x2 operand (the score walk's channel pairs):
+//   [-x0 -x1 -y0 -y1] [a0 a1 2b0 2b1] [c0 c1 t0 t1] [s0 s1 r0 g0] [r1 g1 bl0 bl1]
 struct SoaBatch {
     float4 v[kBatch / 2][5];
 };
@@ -151,9 +152,13 @@ __device__ __forceinline__ void stage_transpose(SoaBatch &s, const RawBatch &raw
         f[0] = f[1] = 0.0f; f[2] = 1.0f; f[3] = 0.0f; f[4] = 1.0f;
         f[5] = __int_as_float(0xff800000); f[6] = f[7] = f[8] = f[9] = 0.0f;
     }
-    float *dst = reinterpret_cast<float *>(&s.v[k >> 1][0]) + (k & 1);
+    float *dst = reinterpret_cast<float *>(&s.v[k >> 1][0]);
+    const int h = k & 1;
 #pragma unroll
-    for (int j = 0; j < 10; ++j) dst[2 * j] = f[j];
+    for (int j = 0; j < 7; ++j) dst[2 * j + h] = f[j];  // -x, -y, a, 2b, c, t, sigma
+    dst[h ? 16 : 14] = f[7];                            // r
+    dst[h ? 17 : 15] = f[8];                            // g
+    dst[18 + h] = f[9];                                 // b
 }
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
@@ -268,7 +273,7 @@ __global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__r
                     if (T1 >= 1e-4f) {  // the even one still blends
                         const float w = al.x * T;
                         C0 = fmaf(v3.z, w, C0);
-                        C1 = fmaf(v4.x, w, C1);
+                        C1 = fmaf(v3.w, w, C1);
                         C2 = fmaf(v4.z, w, C2);
                         T = T1;
                         if (NC) last = al.x > 0.0f ? base + (uint32_t)k : last;
@@ -277,8 +282,8 @@ __global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__r
                     break;
                 }
                 const float2 w = __fmul2_rn(al, make_float2(T, T1));
-                C0 = fmaf(v3.w, w.y, fmaf(v3.z, w.x, C0));
-                C1 = fmaf(v4.y, w.y, fmaf(v4.x, w.x, C1));
+                C0 = fmaf(v4.x, w.y, fmaf(v3.z, w.x, C0));
+                C1 = fmaf(v4.y, w.y, fmaf(v3.w, w.x, C1));
                 C2 = fmaf(v4.w, w.y, fmaf(v4.z, w.x, C2));
                 T = T2;
                 if (NC) last = al.y > 0.0f ? base + (uint32_t)(k + 1) : (al.x > 0.0f ? base + (uint32_t)k : last);
@@ -299,156 +304,197 @@ __global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__r
     if (inside) {
         const float T = st.T[tid];
         const size_t p = (size_t)mpy * W + mpx, plane = (size_t)W * H;
-        out_rgb[p] = fmaf(T, bg0, st.C0[tid]);
-        out_rgb[plane + p] = fmaf(T, bg1, st.C1[tid]);
-        out_rgb[2 * plane + p] = fmaf(T, bg2, st.C2[tid]);
+        if (out_rgb) {  // null: ss_prune_score's forward (T_final and n_contrib only)
+            out_rgb[p] = fmaf(T, bg0, st.C0[tid]);
+            out_rgb[plane + p] = fmaf(T, bg1, st.C1[tid]);
+            out_rgb[2 * plane + p] = fmaf(T, bg2, st.C2[tid]);
+        }
         if (out_T) out_T[p] = T;
         if (NC) out_nc[p] = st.last[tid];
     }
 }
 
-// a7: forward (T_final, last blended index per pixel), then back-to-front over the tile list
-// recovering T_i = T_{i+1} / (1 - alpha_i) and the suffix colour S <- alpha c + (1-alpha) S:
+// a7, second walk (ss_prune_score runs k_render<true> first for T_final and n_contrib per
+// pixel).  Back to front over each pixel's blended entries, T_i = T_{i+1} / (1 - alpha_i) and
+// the suffix colour S <- alpha c + (1 - alpha) S (R19):
 //   dC_ch/dalpha_i = T_i (c_ch - S_ch) - T_final bg_ch / (1 - alpha_i)      (from Eq. 7)
 //   U_i += sum_ch (sigma_i dC_ch/dalpha_i)^2                                 (Eqs. 20-21)
-// Both walks compact the active pixels per batch like k_render.  Per batch, per-Gaussian
-// sums are reduced warp -> CTA in shared memory and added to the float64 score with one
-// atomic per (tile, Gaussian).
-__global__ void __launch_bounds__(256, 6) k_prune_score(const uint2 *__restrict__ ranges,
-                                                     const uint32_t *__restrict__ vals,
-                                                     const float4 *__restrict__ rec, int W, int H, int tiles_x,
-                                                     float bg0, float bg1, float bg2, double *__restrict__ score,
-        const ColorSrc *__restrict__ csp) {
+// Batches are taken from the end of the tile list and staged like k_render's (cp.async ring,
+// pair-interleaved layout, q / alpha of a pair on f32x2); the pixels active in a batch (their
+// last blended entry lies at or after its start) are compacted onto the lowest threads.  The
+// per-Gaussian terms of a warp are summed 8 Gaussians at a time by a transpose-reduce (9
+// shuffles per 8 Gaussians), the warps' sums per Gaussian in shared memory, and one float64
+// atomic per (tile, Gaussian) adds them to the score.
+__global__ void __launch_bounds__(256, 5) k_score_bwd(const uint2 *__restrict__ ranges,
+                                                   const uint32_t *__restrict__ vals,
+                                                   const float4 *__restrict__ rec, int W, int H, int tiles_x,
+                                                   float bg0, float bg1, float bg2,
+                                                   const float *__restrict__ T_final,
+                                                   const uint32_t *__restrict__ n_contrib,
+                                                   double *__restrict__ score, const ColorSrc *__restrict__ csp) {
     pdl_enter();
     const ColorSrc cs = *csp;
-    __shared__ Batch s;
-    __shared__ PixState st;  // forward: T, last, done; backward: T (running), C0..2 = suffix S
+    __shared__ __align__(16) RawBatch raw[2];
+    __shared__ __align__(16) SoaBatch s;
+    __shared__ PixState st;  // T (running), C0..2 = suffix S, last = n_contrib
     __shared__ float s_Tfin[256];
     __shared__ uint32_t s_id[kBatch];
     __shared__ float s_part[8][kBatch];
     __shared__ uint32_t s_warp[8];
     __shared__ uint32_t s_max;
-    const int tile = blockIdx.x;
+    const int tile = blockIdx.x, tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
     int mpx, mpy;
-    tile_pixel(tile, tiles_x, threadIdx.x, mpx, mpy);
+    tile_pixel(tile, tiles_x, tid, mpx, mpy);
     const bool inside = mpx < W && mpy < H;
     const uint2 range = ranges[tile];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    st.T[threadIdx.x] = 1.0f;
-    st.last[threadIdx.x] = 0;
-    st.done[threadIdx.x] = inside ? 0 : 1;
-    if (threadIdx.x == 0) s_max = 0;
-    // forward
-    for (uint32_t start = range.x; start < range.y; start += kBatch) {
-        __syncthreads();
-        const uint32_t n_active = compact_active(!st.done[threadIdx.x], st, s_warp);
-        if (n_active == 0) break;
-        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr, cs);
-        __syncthreads();
-        if (threadIdx.x < n_active) {
-            const int pp = st.list[threadIdx.x];
-            int px, py;
-            tile_pixel(tile, tiles_x, pp, px, py);
-            const float fpx = (float)px, fpy = (float)py;
-            float T = st.T[pp];
-            uint32_t last = st.last[pp];
-            bool done = false;
-            // groups of 4 over the padded batch (padding slots never contribute), as in k_render
-            const int cnt = ((int)min((uint32_t)kBatch, range.y - start) + 3) & ~3;
-            const uint32_t base = start - range.x + 1;
-            for (int k4 = 0; k4 < cnt && !done; k4 += 4)
-#pragma unroll
-            for (int k = k4; k < k4 + 4; ++k) {  // branch-free, as in k_render
-                const float4 bx = s.box[k];
-                const float4 cn = s.con[k];
-                const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
-                const bool contrib = q <= cn.w;
-                const float alpha = contrib ? alpha_of(q, s.col[k].w) : 0.0f;
-                const float Tn = T * (1.0f - alpha);
-                if (Tn < 1e-4f) {
-                    done = true;
-                    break;
-                }
-                T = Tn;
-                last = contrib ? base + (uint32_t)k : last;
-            }
-            st.T[pp] = T;
-            st.last[pp] = last;
-            st.done[pp] = done ? 1 : 0;
-        }
+    if (tid == 0) s_max = 0;
+    const size_t pix = (size_t)mpy * W + mpx;
+    const uint32_t my_last = inside ? n_contrib[pix] : 0u;
+    st.last[tid] = my_last;
+    st.T[tid] = s_Tfin[tid] = inside ? T_final[pix] : 1.0f;
+    st.C0[tid] = st.C1[tid] = st.C2[tid] = 0.0f;
+    __syncthreads();
+    if (my_last) atomicMax(&s_max, my_last);
+    __syncthreads();
+    const uint32_t max_last = min(s_max, range.y - range.x);
+    if (max_last == 0) return;
+    // batch b covers [start_b, end_b), from the end of the blended part of the list
+    const bool loader = tid < kBatch;
+    uint32_t end = range.x + max_last;
+    uint32_t start = end - min((uint32_t)kBatch, max_last);
+    uint32_t g_cur = 0, g_nxt = 0;
+    if (loader) {
+        const uint32_t j0 = start + tid;
+        g_cur = j0 < end ? __ldg(vals + j0) : 0u;
+        const uint32_t s1 = start - min((uint32_t)kBatch, start - range.x), j1 = s1 + tid;
+        g_nxt = j1 < start ? __ldg(vals + j1) : 0u;
+        stage_gather(raw[0], rec, g_cur, j0 < end);
     }
-    __syncthreads();
-    const uint32_t my_last = st.last[threadIdx.x];
-    atomicMax(&s_max, my_last);
-    s_Tfin[threadIdx.x] = st.T[threadIdx.x];
-    st.C0[threadIdx.x] = st.C1[threadIdx.x] = st.C2[threadIdx.x] = 0.0f;
-    __syncthreads();
-    const uint32_t max_last = s_max;
-    // backward, batches from the end; a pixel is active in [start, end) iff last > start
-    for (uint32_t end = range.x + max_last; end > range.x;) {
-        const uint32_t start = end - range.x > (uint32_t)kBatch ? end - kBatch : range.x;
+    cp_async_commit();
+    int buf = 0;
+    const float2 BG01 = make_float2(bg0, bg1);
+    while (end > range.x) {
         const int cnt = (int)(end - start);
-        __syncthreads();
+        __syncthreads();  // the previous batch is consumed: s, s_id, s_part and raw[buf ^ 1] free
+        // the next (earlier) batch in flight, its successor's ids loaded
+        const uint32_t s1 = start - min((uint32_t)kBatch, start - range.x);
+        uint32_t g_after = 0;
+        if (loader) {
+            const uint32_t j1 = s1 + tid;
+            stage_gather(raw[buf ^ 1], rec, g_nxt, j1 < start);
+            const uint32_t s2 = s1 - min((uint32_t)kBatch, s1 - range.x), j2 = s2 + tid;
+            g_after = j2 < s1 ? __ldg(vals + j2) : 0u;
+        }
+        cp_async_commit();
         const uint32_t n_active = compact_active(my_last > start - range.x, st, s_warp);
-        load_batch(s, vals, rec, start + threadIdx.x, end, s_id, cs);
+        cp_async_wait<1>();
+        if (loader) {
+            stage_transpose(s, raw[buf], rec, g_cur, tid < cnt, cs);
+            s_id[tid] = g_cur;
+        }
+        g_cur = g_nxt;
+        g_nxt = g_after;
         __syncthreads();
         const uint32_t n_warps = (n_active + 31) / 32;
         if ((uint32_t)warp < n_warps) {
-            const bool act = threadIdx.x < n_active;
-            const int pp = act ? st.list[threadIdx.x] : 0;
+            const bool act = tid < n_active;
+            const int pp = act ? st.list[tid] : 0;
             int px, py;
             tile_pixel(tile, tiles_x, pp, px, py);
-            const float fpx = (float)px, fpy = (float)py;
+            const float2 FX = f2((float)px), FY = f2((float)py);
             const uint32_t plast = act ? st.last[pp] : 0u;
             const float Tfin = s_Tfin[pp];
             float T = act ? st.T[pp] : 1.0f;
-            // inactive lanes (pp = 0 placeholder) read nothing: pixel 0's state may be written by
-            // its own lane in this phase
-            float S0 = act ? st.C0[pp] : 0.0f, S1 = act ? st.C1[pp] : 0.0f, S2 = act ? st.C2[pp] : 0.0f;
-            for (int k = cnt - 1; k >= 0; --k) {
-                float term = 0.f;
-                if (start - range.x + (uint32_t)k < plast) {
-                    const float4 bx = s.box[k];
-                    const float4 cn = s.con[k];
-                    const float q = pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z);
-                    if (q <= cn.w) {
-                        const float4 cl = s.col[k];
-                        const float alpha = alpha_of(q, cl.w);
-                        const float om = 1.0f - alpha;
-                        float rom;  // T_i = T_{i+1} / (1 - alpha_i): one approximate reciprocal
-                        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rom) : "f"(om));
-                        T = T * rom;
-                        const float bgs = Tfin * rom;
-                        const float d0 = T * (cl.x - S0) - bgs * bg0;
-                        const float d1 = T * (cl.y - S1) - bgs * bg1;
-                        const float d2 = T * (cl.z - S2) - bgs * bg2;
-                        term = cl.w * cl.w * (d0 * d0 + d1 * d1 + d2 * d2);
-                        S0 = alpha * cl.x + om * S0;
-                        S1 = alpha * cl.y + om * S1;
-                        S2 = alpha * cl.z + om * S2;
+            // suffix colour: (S0, S1) as one f32x2, S2 scalar
+            float2 S01 = act ? make_float2(st.C0[pp], st.C1[pp]) : make_float2(0.0f, 0.0f);
+            float S2 = act ? st.C2[pp] : 0.0f;
+            const uint32_t rel = start - range.x;  // list position of slot 0
+            const int top = (cnt + 7) & ~7;          // groups of 8 slots (padding never contributes)
+            for (int k8 = top - 8; k8 >= 0; k8 -= 8) {
+                float tv[8];
+#pragma unroll
+                for (int pq = 3; pq >= 0; --pq) {  // pairs from the top of the group down
+                    const int k = k8 + 2 * pq;
+                    const float4 *v = s.v[k >> 1];
+                    const float4 v0 = v[0], v1 = v[1], v2 = v[2], v3 = v[3], v4 = v[4];
+                    const float2 dx = __fadd2_rn(FX, make_float2(v0.x, v0.y));
+                    const float2 dy = __fadd2_rn(FY, make_float2(v0.z, v0.w));
+                    const float2 u = __ffma2_rn(make_float2(v1.x, v1.y), dx, __fmul2_rn(make_float2(v1.z, v1.w), dy));
+                    const float2 q = __ffma2_rn(dx, u, __fmul2_rn(__fmul2_rn(make_float2(v2.x, v2.y), dy), dy));
+                    const float2 ql = __fmul2_rn(q, f2(-0.72134752044448170f));
+                    const float2 se =
+                        __fmul2_rn(make_float2(v3.x, v3.y), make_float2(ex2_approx(ql.x), ex2_approx(ql.y)));
+#pragma unroll
+                    for (int h = 1; h >= 0; --h) {  // the odd (later) Gaussian first
+                        float term = 0.0f;
+                        const bool blended = rel + (uint32_t)(k + h) < plast && (h ? q.y <= v2.w : q.x <= v2.z);
+                        if (blended) {
+                            const float sg = h ? v3.y : v3.x;
+                            const float alpha = fminf(0.99f, h ? se.y : se.x);
+                            const float2 crg = h ? make_float2(v4.x, v4.y) : make_float2(v3.z, v3.w);
+                            const float cb = h ? v4.w : v4.z;
+                            const float om = 1.0f - alpha;
+                            float rom;  // T_i = T_{i+1} / (1 - alpha_i): one approximate reciprocal
+                            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rom) : "f"(om));
+                            T = T * rom;
+                            const float bgs = Tfin * rom;
+                            // (d0, d1) = T (c_rg - S_rg) - bgs bg_rg on f32x2, d2 scalar
+                            const float2 d01 = __ffma2_rn(f2(-bgs), BG01,
+                                                          __fmul2_rn(f2(T), __fadd2_rn(crg, make_float2(-S01.x, -S01.y))));
+                            const float d2 = T * (cb - S2) - bgs * bg2;
+                            const float2 sq = __fmul2_rn(d01, d01);
+                            term = sg * sg * (sq.x + sq.y + d2 * d2);
+                            S01 = __ffma2_rn(f2(alpha), crg, __fmul2_rn(f2(om), S01));
+                            S2 = alpha * cb + om * S2;
+                        }
+                        tv[2 * pq + h] = term;
                     }
                 }
-                if (__any_sync(0xffffffffu, term != 0.f)) {
+                // warp sums of the 8 terms: transpose-reduce, lane L (L & 3 == 0) ends with the
+                // Gaussian (L >> 2) & 7 of the group
+                bool any = false;
 #pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) term += __shfl_xor_sync(0xffffffffu, term, o);
+                for (int j = 0; j < 8; ++j) any |= tv[j] != 0.0f;
+                if (__any_sync(0xffffffffu, any)) {
+                    const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+                    float v4r[4], v2r[2];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float send = h16 ? tv[j] : tv[4 + j];
+                        v4r[j] = (h16 ? tv[4 + j] : tv[j]) + __shfl_xor_sync(0xffffffffu, send, 16);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const float send = h8 ? v4r[j] : v4r[2 + j];
+                        v2r[j] = (h8 ? v4r[2 + j] : v4r[j]) + __shfl_xor_sync(0xffffffffu, send, 8);
+                    }
+                    float v1 = (h4 ? v2r[1] : v2r[0]) + __shfl_xor_sync(0xffffffffu, h4 ? v2r[0] : v2r[1], 4);
+                    v1 += __shfl_xor_sync(0xffffffffu, v1, 2);
+                    v1 += __shfl_xor_sync(0xffffffffu, v1, 1);
+                    if ((lane & 3) == 0) s_part[warp][k8 + ((lane >> 2) & 7)] = v1;
+                } else if ((lane & 3) == 0) {
+                    s_part[warp][k8 + ((lane >> 2) & 7)] = 0.0f;
                 }
-                if (lane == 0) s_part[warp][k] = term;
             }
             if (act) {
                 st.T[pp] = T;
-                st.C0[pp] = S0;
-                st.C1[pp] = S1;
+                st.C0[pp] = S01.x;
+                st.C1[pp] = S01.y;
                 st.C2[pp] = S2;
             }
         }
         __syncthreads();
-        if ((int)threadIdx.x < cnt) {
+        if (tid < cnt) {
             float sum = 0.f;
-            for (uint32_t w = 0; w < n_warps; ++w) sum += s_part[w][threadIdx.x];
-            if (sum != 0.f) atomicAdd(score + s_id[threadIdx.x], (double)sum);
+            for (uint32_t w = 0; w < n_warps; ++w) sum += s_part[w][tid];
+            if (sum != 0.f) atomicAdd(score + s_id[tid], (double)sum);
         }
         end = start;
+        start = s1;
+        buf ^= 1;
     }
+    cp_async_wait<0>();
 }
 
 // NEXT-2 render backward ("the per-pixel gradients from the render kernel are
@@ -768,9 +814,15 @@ cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg
                                double *score, cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
-    launch_pdl(k_prune_score, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
-                                              at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, score,
-                                              at<const ColorSrc>(ws, L.color_src));
+    // forward walk = k_render with T_final / n_contrib (no image), then the back-to-front walk
+    float *pT = at<float>(ws, L.pix_T);
+    uint32_t *pl = at<uint32_t>(ws, L.pix_last);
+    launch_pdl(k_render<true>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges),
+               at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
+               (float *)nullptr, pT, pl, at<const ColorSrc>(ws, L.color_src));
+    launch_pdl(k_score_bwd, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges),
+               at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
+               (const float *)pT, (const uint32_t *)pl, score, at<const ColorSrc>(ws, L.color_src));
     return cudaGetLastError();
 }
 
