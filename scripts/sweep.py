@@ -1,10 +1,10 @@
 """Frames/s and pairs/frame of every BASELINE.json configuration and tile test (GPU, 1 rank).
 
-    python scripts/sweep.py [--steps 3] [--views 32] > profiles/r01_sweep.jsonl
+    python scripts/sweep.py [--steps 5] [--views 64] [--streams 8] > profiles/r02/r02_sweep.jsonl
 
 One JSON line per (workload, mode): the forward path a1-a6 through the public API, V views
-per step with 3 frames in flight (FramePipeline), K timed steps (CUDA events, L2 flushed
-between steps, 2 warm-up steps), the single-stream per-stage split, plus the
+per step with 8 frames in flight (FramePipeline, one CUDA graph per frame as in bench.py), K
+timed steps (CUDA events, L2 flushed between steps, 2 warm-up steps), the single-stream per-stage split, plus the
 pruned-model regime (BASELINE config 5: U~ over every view, then the prune step removing 90%
 of the Gaussians, AccuTile).  The speed-ups of SnugBox and AccuTile over the 3-sigma baseline
 are the quantities the paper reports as 1.82x / 1.99x on an RTX A5000.
@@ -21,7 +21,7 @@ from paper_2412_00578_b200 import synth  # noqa: E402
 from paper_2412_00578_b200.raster import DeviceScene, FramePipeline, Rasterizer, camera_struct, prune  # noqa: E402
 
 
-def measure(ds, cams, mode, steps, views, streams=3):
+def measure(ds, cams, mode, steps, views, streams=8):
     W, H = cams[0].width, cams[0].height
     rz = Rasterizer(ds, W, H, mode=mode, capacity=max(1024, 4 * ds.n))
     vs = list(range(0, len(cams), max(1, len(cams) // views)))[:views]
@@ -37,12 +37,14 @@ def measure(ds, cams, mode, steps, views, streams=3):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     st = torch.cuda.current_stream()
     pipe = FramePipeline(ds, W, H, mode=mode, n_streams=streams, capacity=rz.capacity)
+    pipe.render_views(cs[:streams])
+    pipe.capture(cs)
     ms = []
     for k in range(steps + 2):
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
-        pipe.render_views(cs)
+        pipe.render_views(cs, graphs=True)
         b.record(st)
         torch.cuda.synchronize()
         if k >= 2:
@@ -70,30 +72,31 @@ def measure(ds, cams, mode, steps, views, streams=3):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--views", type=int, default=32)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--views", type=int, default=64)
+    ap.add_argument("--streams", type=int, default=8)
     args = ap.parse_args()
     for name in ["mnr360-3m", "truck", "garden", "playroom"]:
         scene, cams = synth.make_workload(name)
         ds = DeviceScene.from_host(scene)
         res = {}
         for mode in ["3sigma", "snugbox", "accutile"]:
-            res[mode] = measure(ds, cams, mode, args.steps, args.views)
+            res[mode] = measure(ds, cams, mode, args.steps, args.views, args.streams)
             print(json.dumps({"workload": name, "n": scene.n, "mode": mode, **res[mode]}), flush=True)
         base = res["3sigma"]["fps"]
         print(json.dumps({"workload": name, "speedup_vs_3sigma": {m: res[m]["fps"] / base for m in res},
                           "pairs_ratio_3sigma_over": {m: res["3sigma"]["pairs_per_frame"] / res[m]["pairs_per_frame"]
                                                       for m in res}}), flush=True)
         if True:  # pruned-model regime (BASELINE config 5): score all views, drop 90%, AccuTile
-            rz = Rasterizer(ds, cams[0].width, cams[0].height, mode="accutile", capacity=4 * scene.n)
+            sp = FramePipeline(ds, cams[0].width, cams[0].height, mode="accutile", n_streams=args.streams)
+            sp.ensure_capacity(cams)
             score = torch.zeros(scene.n, dtype=torch.float64, device="cuda")
-            for cam in cams:
-                rz.ensure_capacity(cam)
-                rz.prepare(cam)
-                rz.prune_score(score)
-            del rz
+            sp.score_views(cams, score)
+            torch.cuda.synchronize()
+            sp.check_overflow()
+            del sp
             pds, _ = prune(ds, score, 0.9)
-            r = measure(pds, cams, "accutile", args.steps, args.views)
+            r = measure(pds, cams, "accutile", args.steps, args.views, args.streams)
             print(json.dumps({"workload": name + "-pruned0.9", "n": pds.n, "mode": "accutile", **r,
                               "speedup_vs_unpruned_accutile": r["fps"] / res["accutile"]["fps"]}), flush=True)
         del ds
