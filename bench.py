@@ -243,7 +243,7 @@ def run_ours(args):
         rz = Rasterizer(ds, W, H, mode=args.mode, capacity=max(1024, 8 * ds.n))
 
     # sizing + per-view statistics (untimed): pairs per frame, visible counts, render work
-    pairs, nvis, E_pix, E_blend, E_cta, ncol, dfr = {}, {}, {}, {}, {}, {}, {}
+    pairs, nvis, E_pix, E_blend, E_cta, ncol, dfr, phantom = {}, {}, {}, {}, {}, {}, {}, {}
     for v in my_views:
         rz.ensure_capacity(cams[v])
     cap = rz.capacity
@@ -255,7 +255,7 @@ def run_ours(args):
         pairs[v], nvis[v], dfr[v] = t["pairs"], t["n_visible"], t["deferred"]
         ncol[v] = int(((rz.records()[:, 8] == 1.0) & (rz.depth_keys() != -1)).sum().item())
         st = rz.render_stats()
-        E_pix[v], E_blend[v], E_cta[v] = st["E_pix"], st["E_blend"], st["E_cta"]
+        E_pix[v], E_blend[v], E_cta[v], phantom[v] = st["E_pix"], st["E_blend"], st["E_cta"], st["phantom_pairs"]
     # shrink capacity to the measured maximum (+2%) so the per-frame memset is tight
     rz._alloc(int(max(pairs.values()) * 1.02) + 4096)
 
@@ -667,6 +667,9 @@ def run_ours(args):
             "stages": stage_info,
             "render_work": {"E_pix": mean(E_pix), "E_blend": mean(E_blend), "E_cta": mean(E_cta),
                             "pixels": W * H},
+            "phantom_tiles": {"per_frame": mean(phantom), "rate": mean(phantom) / Pm,
+                              "note": "(tile, Gaussian) pairs whose Gaussian has alpha < 1/255 at every pixel centre "
+                                      "of the tile (AccuTile tests the continuous cell, DESIGN.md R23)"},
             "stages_timing": "single-stream pass of V frames after the timed region (every stage bracketed by events)",
             "roofline": roof,
             # ours per frame: k_preprocess, 4 x k_onesweep, k_escan_reduce, k_escan_apply, k_entries,

@@ -224,8 +224,9 @@ SS_API ss_status ss_finalize_colours(const ss_frame *frame /*host*/, void *strea
 /* Measurement helper (never on the timed path): work counts of ss_render for the frame,
  * accumulated into counters (device uint64 [5]): E_pix (per-pixel evaluations until each
  * pixel terminates: the method's work), E_blend (evaluations that blend), E_cta (evaluations
- * issued by CTA-lock-step walking: 256 x Gaussians staged per tile), pixels, and a reserved
- * slot (always 0). */
+ * issued by CTA-lock-step walking: 256 x Gaussians staged), pixels, and phantom pairs ((tile,
+ * Gaussian) pairs whose Gaussian has alpha < 1/255 at every pixel centre of the tile; AccuTile
+ * tests the continuous cell, R23). */
 SS_API ss_status ss_render_stats(const ss_frame *frame /*host*/, uint64_t *counters, void *stream);
 
 /* a7 -- efficient pruning score (Sec. 4.2.1, Eqs. 20-21):

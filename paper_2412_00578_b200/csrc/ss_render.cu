@@ -28,6 +28,14 @@ constexpr int kBatch = 128;
 #define SS_RENDER_UNROLL 2
 #endif
 constexpr int kRenderUnroll = SS_RENDER_UNROLL;  // pairs per k_render loop iteration
+#ifndef SS_RENDER_PIX
+#define SS_RENDER_PIX 256
+#endif
+#ifndef SS_RENDER_BATCH
+#define SS_RENDER_BATCH 128
+#endif
+constexpr int kRenderPix = SS_RENDER_PIX;      // pixels per k_render CTA (256: a tile, 128: half a tile)
+constexpr int kRenderBatch = SS_RENDER_BATCH;  // Gaussians per k_render batch
 
 // Shared-memory batch of gathered records, split by use: the per-warp culling box, the conic
 // (skip test), the colour.
@@ -80,12 +88,14 @@ __device__ __forceinline__ void tile_pixel(int tile, int tiles_x, int p, int &px
 // still-active pixels can be compacted onto the lowest threads: warps whose pixels have all
 // terminated stop issuing, instead of idling lane by lane inside partially-done warps
 // (the per-pixel walk and its arithmetic are unchanged).
-struct PixState {
-    float T[256], C0[256], C1[256], C2[256];
-    uint32_t last[256];
-    uint8_t done[256];
-    uint16_t list[256];
+template <int PIX>
+struct PixStateT {
+    float T[PIX], C0[PIX], C1[PIX], C2[PIX];
+    uint32_t last[PIX];
+    uint8_t done[PIX];
+    uint16_t list[PIX];
 };
+using PixState = PixStateT<256>;
 
 // Compacts the active pixels (one flag per thread = pixel threadIdx.x) into st.list; returns
 // their number.  Every thread of the CTA must call it.
@@ -103,16 +113,20 @@ __device__ __forceinline__ uint32_t compact_active(bool active, PixState &st, ui
 // a batch has landed its loader thread transposes its slot into structure-of-arrays form
 // (computing a pending colour, ss_color.cuh), so that one 128-bit shared load gives a field of
 // four consecutive Gaussians and consecutive pairs feed the packed FP32 pipe (f32x2).
-struct RawBatch {
-    float4 q[3 * kBatch];  // records as gathered: q0, q1, q2 per slot
+template <int B>
+struct RawBatchT {
+    float4 q[3 * B];  // records as gathered: q0, q1, q2 per slot
 };
+using RawBatch = RawBatchT<kBatch>;
 // Pair-interleaved (AoSoA) layout: Gaussians 2p and 2p+1 share 20 floats, so that one 128-bit
 // shared load gives two fields of the pair as two f32x2 operands, and the (r, g) of each
 // Gaussian as one f32x2 operand (the score walk's channel pairs):
 //   [-x0 -x1 -y0 -y1] [a0 a1 2b0 2b1] [c0 c1 t0 t1] [s0 s1 r0 g0] [r1 g1 bl0 bl1]
-struct SoaBatch {
-    float4 v[kBatch / 2][5];
+template <int B>
+struct SoaBatchT {
+    float4 v[B / 2][5];
 };
+using SoaBatch = SoaBatchT<kBatch>;
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -123,7 +137,8 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // Slot threadIdx.x (< kBatch) of a batch: issue the gather of Gaussian g's record.
-__device__ __forceinline__ void stage_gather(RawBatch &raw, const float4 *__restrict__ rec, uint32_t g, bool valid) {
+template <int B>
+__device__ __forceinline__ void stage_gather(RawBatchT<B> &raw, const float4 *__restrict__ rec, uint32_t g, bool valid) {
     if (valid) {
         const float4 *src = rec + 3 * (size_t)g;
         cp_async16(&raw.q[3 * threadIdx.x + 0], src + 0);
@@ -134,7 +149,8 @@ __device__ __forceinline__ void stage_gather(RawBatch &raw, const float4 *__rest
 
 // Slot threadIdx.x (< kBatch): raw record -> pair-interleaved layout (padding slots never
 // contribute: q <= -inf is false); a pending colour is computed here and stored back.
-__device__ __forceinline__ void stage_transpose(SoaBatch &s, const RawBatch &raw, const float4 *rec, uint32_t g,
+template <int B>
+__device__ __forceinline__ void stage_transpose(SoaBatchT<B> &s, const RawBatchT<B> &raw, const float4 *rec, uint32_t g,
                                                 bool valid, const ColorSrc &cs) {
     const int k = threadIdx.x;
     float f[10];
@@ -168,32 +184,36 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return e;
 }
 
-template <bool NC>  // NC: track the last blended list entry per pixel (out_ncontrib requested)
-__global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
+// PIX pixels per CTA (256: a whole tile; 128: half a tile, rows 8 h .. 8 h + 7 of tile
+// blockIdx.x / 2, so that fewer warps wait at each batch barrier), B Gaussians per batch.
+template <bool NC, int PIX, int B>  // NC: track the last blended list entry per pixel (out_ncontrib)
+__global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
                                                 const float4 *__restrict__ rec, int W, int H, int tiles_x, float bg0,
                                                 float bg1, float bg2, float *__restrict__ out_rgb,
                                                 float *__restrict__ out_T, uint32_t *__restrict__ out_nc,
         const ColorSrc *__restrict__ csp) {
     pdl_enter();
     const ColorSrc cs = *csp;
-    __shared__ __align__(16) RawBatch raw[2];
-    __shared__ __align__(16) SoaBatch s;
-    __shared__ PixState st;
-    __shared__ uint32_t s_warp[8];
-    const int tile = blockIdx.x;
+    constexpr int NW = PIX / 32;
+    __shared__ __align__(16) RawBatchT<B> raw[2];
+    __shared__ __align__(16) SoaBatchT<B> s;
+    __shared__ PixStateT<PIX> st;
+    __shared__ uint32_t s_warp[NW];
+    const int tile = PIX == 256 ? blockIdx.x : blockIdx.x >> 1;
+    const int p0 = PIX == 256 ? 0 : (blockIdx.x & 1) * PIX;  // first tile pixel of this CTA
     const int tid = threadIdx.x;
     int mpx, mpy;
-    tile_pixel(tile, tiles_x, tid, mpx, mpy);
+    tile_pixel(tile, tiles_x, p0 + tid, mpx, mpy);
     const bool inside = mpx < W && mpy < H;
     const uint2 range = ranges[tile];
     st.T[tid] = 1.0f;
     st.C0[tid] = st.C1[tid] = st.C2[tid] = 0.0f;
     st.last[tid] = 0;
     // ids of batches 0 and 1 of this slot; batch 0 gathered before the loop
-    const bool loader = tid < kBatch;
+    const bool loader = tid < B;
     uint32_t g_cur = 0, g_nxt = 0;
     if (loader) {
-        const uint32_t j0 = range.x + tid, j1 = j0 + kBatch;
+        const uint32_t j0 = range.x + tid, j1 = j0 + B;
         g_cur = j0 < range.y ? __ldg(vals + j0) : 0u;
         g_nxt = j1 < range.y ? __ldg(vals + j1) : 0u;
         stage_gather(raw[0], rec, g_cur, j0 < range.y);
@@ -208,11 +228,11 @@ __global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__r
     uint32_t bal = __ballot_sync(0xffffffffu, my_act);
     if ((tid & 31) == 0) s_warp[tid >> 5] = __popc(bal);
     int buf = 0;
-    for (uint32_t start = range.x; start < range.y; start += kBatch, buf ^= 1) {
+    for (uint32_t start = range.x; start < range.y; start += B, buf ^= 1) {
         __syncthreads();  // the previous walk is done: s, raw[buf ^ 1] free; warp counts visible
         uint32_t n_active = 0, pos = 0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
+        for (int w = 0; w < NW; ++w) {
             const uint32_t c = s_warp[w];
             pos += w < (tid >> 5) ? c : 0u;
             n_active += c;
@@ -221,7 +241,7 @@ __global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__r
         if (my_act) st.list[pos + __popc(bal & ((1u << (tid & 31)) - 1u))] = (uint16_t)my_pp;
         uint32_t g_after = 0;
         if (loader) {
-            const uint32_t j1 = start + kBatch + tid, j2 = j1 + kBatch;
+            const uint32_t j1 = start + B + tid, j2 = j1 + B;
             stage_gather(raw[buf ^ 1], rec, g_nxt, j1 < range.y);           // batch b+1, in flight
             g_after = j2 < range.y ? __ldg(vals + j2) : 0u;                 // id of batch b+2
         }
@@ -235,7 +255,7 @@ __global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__r
         if (tid < n_active) {
             const int pp = st.list[tid];
             int px, py;
-            tile_pixel(tile, tiles_x, pp, px, py);
+            tile_pixel(tile, tiles_x, p0 + pp, px, py);
             const float2 FX = f2((float)px), FY = f2((float)py);
             float T = st.T[pp], C0 = st.C0[pp], C1 = st.C1[pp], C2 = st.C2[pp];
             uint32_t last = st.last[pp];
@@ -249,7 +269,7 @@ __global__ void __launch_bounds__(256, SS_RENDER_MINB) k_render(const uint2 *__r
             // The colour sums stay sequential (C += c alpha T in list order), so the image is
             // bit-identical to a one-by-one walk: AccuTile and SnugBox renders stay bitwise equal
             // (their lists differ only by Gaussians with alpha = 0 everywhere in the tile).
-            const int cnt = ((int)min((uint32_t)kBatch, range.y - start) + 1) & ~1;
+            const int cnt = ((int)min((uint32_t)B, range.y - start) + 1) & ~1;
             const uint32_t base = start - range.x + 1;
 #pragma unroll kRenderUnroll
             for (int k = 0; k < cnt; k += 2) {
@@ -689,7 +709,9 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
 // the same per-pixel walk as k_render.  counters[0] += E_pix (evaluations each pixel makes
 // until it terminates, the method's work), [1] += E_blend (evaluations that blend),
 // [2] += E_cta (evaluations a CTA issues in lock-step until its last pixel terminates:
-// 256 x Gaussians staged), [3] += pixels; [4] is reserved (left 0).
+// 256 x Gaussians staged), [3] += pixels, [4] += phantom pairs: (tile, Gaussian) pairs of the
+// list whose Gaussian has q > t (alpha < 1/255) at every pixel centre of the tile (AccuTile's
+// tile test is against the continuous cell, R23; this walks every pair, no termination).
 __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ ranges,
                                                       const uint32_t *__restrict__ vals,
                                                       const float4 *__restrict__ rec, int W, int H, int tiles_x,
@@ -731,6 +753,25 @@ __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ 
             T = Tn;
         }
     }
+    // phantom pairs: every batch of the list against every pixel centre of the tile
+    unsigned long long phantom = 0;
+    __shared__ uint32_t s_hit[kBatch / 32];
+    for (uint32_t start = range.x; start < range.y; start += kBatch) {
+        __syncthreads();
+        load_batch(s, vals, rec, start + threadIdx.x, range.y, nullptr, cs);
+        if (threadIdx.x < kBatch / 32) s_hit[threadIdx.x] = 0;
+        __syncthreads();
+        const int cnt = min((uint32_t)kBatch, range.y - start);
+        for (int k = 0; k < cnt; ++k) {
+            const float4 bx = s.box[k];
+            const float4 cn = s.con[k];
+            const bool hit = inside && pixel_q(fpx, fpy, bx.x, bx.y, cn.x, cn.y, cn.z) <= cn.w;
+            if (__any_sync(0xffffffffu, hit) && (threadIdx.x & 31) == 0) atomicOr(&s_hit[k >> 5], 1u << (k & 31));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int k = 0; k < cnt; ++k) phantom += (s_hit[k >> 5] >> (k & 31)) & 1u ? 0u : 1u;
+    }
     __syncthreads();
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -748,6 +789,7 @@ __global__ void __launch_bounds__(256) k_render_stats(const uint2 *__restrict__ 
         atomicAdd(counters + 1, s_acc[1]);
         atomicAdd(counters + 2, e_cta * blockDim.x);
         atomicAdd(counters + 3, (unsigned long long)n_inside);
+        atomicAdd(counters + 4, phantom);
     }
 }
 
@@ -784,14 +826,15 @@ cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, fl
                           float *out_T, uint32_t *out_nc, cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
+    const int grid = P.n_tiles * (256 / kRenderPix);
     if (out_nc)
-        launch_pdl(k_render<true>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
-                                                   at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
-                                                   out_T, out_nc, at<const ColorSrc>(ws, L.color_src));
+        launch_pdl(k_render<true, kRenderPix, kRenderBatch>, grid, kRenderPix, 0, st, at<const uint2>(ws, P.ranges),
+                   at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
+                   out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src));
     else
-        launch_pdl(k_render<false>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value),
-                                                    at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2, out_rgb,
-                                                    out_T, out_nc, at<const ColorSrc>(ws, L.color_src));
+        launch_pdl(k_render<false, kRenderPix, kRenderBatch>, grid, kRenderPix, 0, st, at<const uint2>(ws, P.ranges),
+                   at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
+                   out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src));
     return cudaGetLastError();
 }
 
@@ -817,9 +860,9 @@ cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg
     // forward walk = k_render with T_final / n_contrib (no image), then the back-to-front walk
     float *pT = at<float>(ws, L.pix_T);
     uint32_t *pl = at<uint32_t>(ws, L.pix_last);
-    launch_pdl(k_render<true>, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges),
-               at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
-               (float *)nullptr, pT, pl, at<const ColorSrc>(ws, L.color_src));
+    launch_pdl(k_render<true, kRenderPix, kRenderBatch>, P.n_tiles * (256 / kRenderPix), kRenderPix, 0, st,
+               at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W,
+               H, P.tiles_x, bg0, bg1, bg2, (float *)nullptr, pT, pl, at<const ColorSrc>(ws, L.color_src));
     launch_pdl(k_score_bwd, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges),
                at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
                (const float *)pT, (const uint32_t *)pl, score, at<const ColorSrc>(ws, L.color_src));

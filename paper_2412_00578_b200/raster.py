@@ -198,7 +198,7 @@ class Rasterizer:
         check(lib().ss_render_stats(C.byref(self.frame), C.c_void_p(c.data_ptr()),
                                     C.c_void_p(_stream_handle(stream))), "ss_render_stats")
         v = c.cpu().tolist()
-        return {"E_pix": v[0], "E_blend": v[1], "E_cta": v[2], "pixels": v[3]}
+        return {"E_pix": v[0], "E_blend": v[1], "E_cta": v[2], "pixels": v[3], "phantom_pairs": v[4]}
 
     def prune_score(self, score: torch.Tensor, bg=(0.0, 0.0, 0.0), stream=None) -> torch.Tensor:
         assert score.dtype == torch.float64 and score.numel() == self.scene.n and score.is_cuda

@@ -181,3 +181,24 @@ def test_edge_cases():
     _check_frame(scene.subset(np.array([123])), cam, "accutile")
     # overflow: tiny capacity, then render_frame regrows and re-runs
     _check_frame(scene, cam, "accutile", capacity=8)
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny-lowsigma"])
+def test_phantom_pairs_invariant(name):
+    """ss_render_stats' phantom pairs (a Gaussian's tile with alpha < 1/255 at every pixel
+    centre): the pairs that DO hit a pixel centre are the same set in every mode whose tile sets
+    contain every pixel-hit tile -- SnugBox and AccuTile (R23: pixel-hit <= AccuTile <=
+    SnugBox) -- so P - phantom is equal for both, and AccuTile has no more phantoms."""
+    from paper_2412_00578_b200.raster import DeviceScene, Rasterizer
+    scene, cams = synth.make_workload(name)
+    cam = cams[0]
+    ds = DeviceScene.from_host(scene)
+    res = {}
+    for mode in ("snugbox", "accutile"):
+        rz = Rasterizer(ds, cam.width, cam.height, mode=mode)
+        rz.render_frame(cam)
+        st = rz.render_stats()
+        res[mode] = (rz.totals()["pairs"], st["phantom_pairs"])
+    (ps, fs), (pa, fa) = res["snugbox"], res["accutile"]
+    assert 0 <= fa <= fs and fa < pa
+    assert ps - fs == pa - fa, res
