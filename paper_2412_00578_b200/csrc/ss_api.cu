@@ -194,7 +194,9 @@ ss_status ss_bin(const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame, 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaMemsetAsync(at<char>(frame->ws, L.zero_bin), 0, L.zero_bin_end - L.zero_bin, st);
     if (e == cudaSuccess) e = launch_depth_sort(frame->ws, L, st);
+#ifndef SS_DIAG_BIN_STAGES  // diagnostics builds only: stop ss_bin after the depth sort
     if (e == cudaSuccess) e = launch_bin(frame->ws, L, st);
+#endif
     return cuda_status(e);
 }
 

@@ -732,6 +732,9 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
                at<const uint32_t>(ws, P.total_pairs), L.capacity, ctr + 8, at<uint32_t>(ws, P.overflow),
                at<uint32_t>(ws, P.overflow_count));
     if (L.nck_max == 0) return cudaGetLastError();
+#if defined(SS_DIAG_BIN_UPTO) && SS_DIAG_BIN_UPTO == 2
+    return cudaGetLastError();
+#endif
     const uint32_t *E = ctr + 8;
     int sbits = 1;
     while ((1 << sbits) < L.n_super) ++sbits;
@@ -744,6 +747,9 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
                                            at<const uint32_t>(ws, P.order), at<const uint4>(ws, P.erec),
                                            at<const float4>(ws, P.rec), P.tiles_x, P.tiles_y, L.stx,
                                            at<uint2>(ws, L.stg));
+#if defined(SS_DIAG_BIN_UPTO) && SS_DIAG_BIN_UPTO == 3
+    return cudaGetLastError();
+#endif
     const size_t smem = l1_smem_bytes(L.n_super);
     cudaError_t e = cudaSuccess;
     switch (sbits <= 8 ? 8 : sbits) {
@@ -754,6 +760,9 @@ cudaError_t launch_bin(void *ws, const Layout &L, cudaStream_t st) {
         default: e = launch_level1<12>(ws, L, smem, E, ctr, st); break;
     }
     if (e != cudaSuccess) return e;
+#if defined(SS_DIAG_BIN_UPTO) && SS_DIAG_BIN_UPTO == 4
+    return cudaGetLastError();
+#endif
     launch_pdl(k_l2_count, L.l2_max_blocks, kL2Threads, 0, st, 
         at<const uint32_t>(ws, P.overflow), L.stx, P.tiles_x, P.tiles_y, L.n_super, at<const uint32_t>(ws, L.st_total),
         at<const uint32_t>(ws, L.st_base), at<const uint32_t>(ws, L.st_blk0), at<const uint2>(ws, L.l2_blocks),
