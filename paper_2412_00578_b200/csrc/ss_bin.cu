@@ -136,20 +136,43 @@ __device__ __forceinline__ void put_entry(uint2 *__restrict__ stg, uint32_t e, u
 }
 
 // Entries of a Gaussian whose line spans are stored in its emission record (AccuTile, at most
-// kLaneRows lines): the band accumulator over the spans, in the count's order.
+// kLaneRows lines, non-empty lines in increasing order): per band of 4 lines, one entry for
+// every super-tile between the band's span extremes, its mask the union of the band's spans
+// there (bit (y & 3) * 4 + (x & 3)) -- the entries band_entries emits (ss_tilegeom.cuh), in
+// its order, computed directly from the spans.
 __device__ __forceinline__ void span_entries(uint2 *__restrict__ stg, uint32_t g, uint32_t eo, uint32_t info,
                                              const uint4 &e0, const uint4 &e1, int stx) {
     const uint32_t v[6] = {e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
-    const uint32_t ns = info & 0xFFu;
-    EntryAcc acc;
-    acc_init(acc, (info & kInfoCols) != 0, stx);
+    const int ns = (int)(info & 0xFFu);
+    const bool cols = (info & kInfoCols) != 0;
     uint32_t e = eo;
-    auto out = [&](uint32_t st, uint32_t mask) { put_entry(stg, e++, st, g, mask); };
+    int q = 0;
 #pragma unroll 1
-    for (int q = 0; q < 6; ++q)
-        if ((uint32_t)q < ns)
-            acc_feed(acc, (int)(v[q] >> 18), (int)(v[q] & 0x1FFu), (int)((v[q] >> 9) & 0x1FFu), out);
-    acc_flush(acc, out);
+    while (q < ns) {
+        const int band = (int)(v[q] >> 20);  // line >> 2 (line = bits 18..)
+        int lo = (int)(v[q] & 0x1FFu), hi = (int)((v[q] >> 9) & 0x1FFu);
+        int q2 = q + 1;
+#pragma unroll 1
+        for (; q2 < ns && (int)(v[q2] >> 20) == band; ++q2) {
+            lo = min(lo, (int)(v[q2] & 0x1FFu));
+            hi = max(hi, (int)((v[q2] >> 9) & 0x1FFu));
+        }
+#pragma unroll 1
+        for (int C = lo >> 2; C <= (hi - 1) >> 2; ++C) {
+            uint32_t mask = 0;
+#pragma unroll 1
+            for (int s = q; s < q2; ++s) {
+                const int a = max((int)(v[s] & 0x1FFu), 4 * C), b = min((int)((v[s] >> 9) & 0x1FFu), 4 * C + 4);
+                if (b > a) {
+                    const uint32_t bits = ((1u << (b - a)) - 1u) << (a - 4 * C);
+                    const int r = (int)(v[s] >> 18) & 3;
+                    mask |= cols ? (spread4(bits) << r) : (bits << (4 * r));
+                }
+            }
+            put_entry(stg, e++, cols ? (uint32_t)(C * stx + band) : (uint32_t)(band * stx + C), g, mask);
+        }
+        q = q2;
+    }
 }
 
 // Entries of a Gaussian with at most kInlineEnt entries: copied from its emission record.
