@@ -25,7 +25,10 @@ struct CamArgs {
 
 // Depth-sort geometry (onesweep LSD radix sort).
 constexpr int kSortThreads = 256;
-constexpr int kSortItems = 12;
+#ifndef SS_SORT_ITEMS
+#define SS_SORT_ITEMS 12
+#endif
+constexpr int kSortItems = SS_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 3072 keys per block tile
 constexpr int kInlineEnt = 6;                          // super-tile entries stored in the emission record
 constexpr int kLaneRows = 6;                           // AccuTile lines a preprocess lane sweeps alone

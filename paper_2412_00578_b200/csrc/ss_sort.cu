@@ -25,7 +25,7 @@ constexpr int kLBSleepNs = SS_SORT_SLEEP;
 #define SS_SORT_GRID 4  // persistent onesweep CTAs per SM
 #endif
 #ifndef SS_SORT_MATCH
-#define SS_SORT_MATCH 0
+#define SS_SORT_MATCH 1
 #endif  // back-off when no predecessor has published yet
 
 template <typename K>
@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(kSortThreads, 4) k_onesweep(const K *__restric
             const bool valid = idx < n && (!FILTER || key[j] != kNoTiles);
             const uint32_t d = digit_of(key[j], shift);
 #if SS_SORT_MATCH
-            const uint32_t peers = valid ? __match_any_sync(0xffffffffu, valid ? d : 256u + (uint32_t)lane) : 0u;
+            uint32_t peers = __match_any_sync(0xffffffffu, valid ? d : 256u + (uint32_t)lane);
+            peers = valid ? peers : 0u;
 #else
             uint32_t peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
