@@ -15,6 +15,10 @@
 // uses the pinned chain u = fma(a, dx, (2b) dy); q = fma(dx, u, (c dy) dy) with explicit
 // round-to-nearest intrinsics, so it is bit-identical to the oracle's; alpha uses the SFU
 // exp2 (ex2.approx), which the image tolerance (1e-4) covers.
+#include <cstring>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ss_color.cuh"
 
 namespace ss {
@@ -36,6 +40,10 @@ constexpr int kRenderUnroll = SS_RENDER_UNROLL;  // pairs per k_render loop iter
 #endif
 constexpr int kRenderPix = SS_RENDER_PIX;      // pixels per k_render CTA (256: a tile, 128: half a tile)
 constexpr int kRenderBatch = SS_RENDER_BATCH;  // Gaussians per k_render batch
+#ifndef SS_RENDER_TMA
+#define SS_RENDER_TMA 0
+#endif
+constexpr bool kRenderTma = SS_RENDER_TMA != 0;  // batch staging by TMA gather4 (else cp.async)
 
 // Shared-memory batch of gathered records, split by use: the per-warp culling box, the conic
 // (skip test), the colour.
@@ -150,13 +158,13 @@ __device__ __forceinline__ void stage_gather(RawBatchT<B> &raw, const float4 *__
 // Slot threadIdx.x (< kBatch): raw record -> pair-interleaved layout (padding slots never
 // contribute: q <= -inf is false); a pending colour is computed here and stored back.
 template <int B>
-__device__ __forceinline__ void stage_transpose(SoaBatchT<B> &s, const RawBatchT<B> &raw, const float4 *rec, uint32_t g,
-                                                bool valid, const ColorSrc &cs) {
+__device__ __forceinline__ void stage_transpose_rows(SoaBatchT<B> &s, const float4 *row, const float4 *rec, uint32_t g,
+                                                     bool valid, const ColorSrc &cs) {
     const int k = threadIdx.x;
     float f[10];
     if (valid) {
-        const float4 q0 = raw.q[3 * k + 0], q1 = raw.q[3 * k + 1];
-        float4 q2 = raw.q[3 * k + 2];
+        const float4 q0 = row[0], q1 = row[1];
+        float4 q2 = row[2];
         if (q2.x == 0.0f) {  // pending colour: computed by this gather (the same value every time)
             const float3 c = sh_color(cs, g);
             q2 = make_float4(1.0f, c.x, c.y, c.z);
@@ -177,6 +185,43 @@ __device__ __forceinline__ void stage_transpose(SoaBatchT<B> &s, const RawBatchT
     dst[18 + h] = f[9];                                 // b
 }
 
+template <int B>
+__device__ __forceinline__ void stage_transpose(SoaBatchT<B> &s, const RawBatchT<B> &raw, const float4 *rec, uint32_t g,
+                                                bool valid, const ColorSrc &cs) {
+    stage_transpose_rows(s, &raw.q[3 * threadIdx.x], rec, g, valid, cs);
+}
+
+// ---- TMA (cp.async.bulk.tensor ... tile::gather4) staging of a batch: one warp issues B / 4
+// gathers of 4 record rows (48 B each) into 256 B-aligned slots of a buffer; an mbarrier per
+// buffer counts the bytes.
+template <int B>
+struct TmaBatchT {
+    float4 q[B / 4][16];  // 4 rows x 3 float4 per gather, padded to 256 B
+};
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *m, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *m, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(m)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, uint64_t *m, int r0, int r1, int r2,
+                                            int r3) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(smem_u32(m)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+        : "memory");
+}
+
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
 __device__ __forceinline__ float ex2_approx(float x) {
     float e;
@@ -186,16 +231,21 @@ __device__ __forceinline__ float ex2_approx(float x) {
 
 // PIX pixels per CTA (256: a whole tile; 128: half a tile, rows 8 h .. 8 h + 7 of tile
 // blockIdx.x / 2, so that fewer warps wait at each batch barrier), B Gaussians per batch.
-template <bool NC, int PIX, int B>  // NC: track the last blended list entry per pixel (out_ncontrib)
+// TMA: stage the batches with cp.async.bulk.tensor ... tile::gather4 (UTMALDG; one warp issues
+// the B / 4 gathers of a batch, an mbarrier per buffer) instead of per-slot cp.async (LDGSTS).
+template <bool NC, int PIX, int B, bool TMA>  // NC: track the last blended list entry per pixel (out_ncontrib)
 __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(const uint2 *__restrict__ ranges, const uint32_t *__restrict__ vals,
                                                 const float4 *__restrict__ rec, int W, int H, int tiles_x, float bg0,
                                                 float bg1, float bg2, float *__restrict__ out_rgb,
                                                 float *__restrict__ out_T, uint32_t *__restrict__ out_nc,
-        const ColorSrc *__restrict__ csp) {
+        const ColorSrc *__restrict__ csp, const __grid_constant__ CUtensorMap tmap) {
     pdl_enter();
     const ColorSrc cs = *csp;
     constexpr int NW = PIX / 32;
-    __shared__ __align__(16) RawBatchT<B> raw[2];
+    __shared__ __align__(16) RawBatchT<TMA ? 4 : B> raw[2];
+    __shared__ __align__(256) TmaBatchT<TMA ? B : 4> tb[2];
+    __shared__ uint32_t s_gid[2][TMA ? B : 1];
+    __shared__ __align__(8) uint64_t s_mbar[2];
     __shared__ __align__(16) SoaBatchT<B> s;
     __shared__ PixStateT<PIX> st;
     __shared__ uint32_t s_warp[NW];
@@ -212,13 +262,49 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
     // ids of batches 0 and 1 of this slot; batch 0 gathered before the loop
     const bool loader = tid < B;
     uint32_t g_cur = 0, g_nxt = 0;
-    if (loader) {
-        const uint32_t j0 = range.x + tid, j1 = j0 + B;
-        g_cur = j0 < range.y ? __ldg(vals + j0) : 0u;
-        g_nxt = j1 < range.y ? __ldg(vals + j1) : 0u;
-        stage_gather(raw[0], rec, g_cur, j0 < range.y);
+    uint32_t g4[4] = {0u, 0u, 0u, 0u};  // TMA: warp 0 lane l holds the ids of slots 4l..4l+3 of the next batch
+    const int lane = tid & 31;
+    // TMA: warp 0 stages the batch at list position bs (ids in g4) into buffer sb
+    auto tma_issue = [&](uint32_t bs, int sb) {
+        const uint32_t n_slots = min((uint32_t)B, range.y - bs);
+        const uint32_t n_g = (n_slots + 3) / 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s_gid[sb][4 * lane + q] = g4[q];
+        if (lane == 0) mbar_expect_tx(&s_mbar[sb], n_g * 192u);
+        __syncwarp();
+        if ((uint32_t)lane < n_g) tma_gather4(&tb[sb].q[lane][0], &tmap, &s_mbar[sb], (int)g4[0], (int)g4[1], (int)g4[2], (int)g4[3]);
+    };
+    auto tma_load_ids = [&](uint32_t bs) {  // ids of the batch at bs (invalid slots repeat a valid id)
+        const uint32_t n_slots = bs < range.y ? min((uint32_t)B, range.y - bs) : 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t k = 4 * lane + q;
+            g4[q] = k < n_slots ? __ldg(vals + bs + k) : (n_slots ? __ldg(vals + bs) : 0u);
+        }
+    };
+    if constexpr (TMA) {
+        if (tid == 0) {
+            mbar_init(&s_mbar[0], 1);
+            mbar_init(&s_mbar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (tid < 32) {
+            tma_load_ids(range.x);
+            if (range.x < range.y) tma_issue(range.x, 0);
+            tma_load_ids(range.x + B);  // the next batch's ids
+        }
+    } else {
+        if (loader) {
+            const uint32_t j0 = range.x + tid, j1 = j0 + B;
+            g_cur = j0 < range.y ? __ldg(vals + j0) : 0u;
+            g_nxt = j1 < range.y ? __ldg(vals + j1) : 0u;
+            stage_gather(raw[0], rec, g_cur, j0 < range.y);
+        }
+        cp_async_commit();
     }
-    cp_async_commit();
+    uint32_t n_uses = 0;     // TMA: batches staged into buffer 0 / 1 so far (parity of the next wait)
+    bool in_flight = false;  // TMA: a batch issued but not consumed when the loop ends
     // Pixel compaction, two barriers per batch: every thread carries the pixel it walked (my_pp)
     // and whether it is still active (my_act); per-warp counts of the active ones are published
     // with the barrier that ends the walk, and the next list (stable: pixel-index order) is
@@ -239,17 +325,32 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
         }
         if (n_active == 0) break;
         if (my_act) st.list[pos + __popc(bal & ((1u << (tid & 31)) - 1u))] = (uint16_t)my_pp;
-        uint32_t g_after = 0;
-        if (loader) {
-            const uint32_t j1 = start + B + tid, j2 = j1 + B;
-            stage_gather(raw[buf ^ 1], rec, g_nxt, j1 < range.y);           // batch b+1, in flight
-            g_after = j2 < range.y ? __ldg(vals + j2) : 0u;                 // id of batch b+2
+        if constexpr (TMA) {
+            in_flight = start + B < range.y;
+            if (tid < 32 && in_flight) {
+                tma_issue(start + B, buf ^ 1);  // batch b+1, in flight
+                tma_load_ids(start + 2 * B);    // ids of batch b+2
+            }
+            if (loader) {
+                mbar_wait(&s_mbar[buf], (n_uses >> 1) & 1u);  // batch b has landed (buffer buf, use n_uses / 2)
+                const int k = tid;
+                const float4 *row = &tb[buf].q[k >> 2][(k & 3) * 3];
+                stage_transpose_rows(s, row, rec, s_gid[buf][k], start + tid < range.y, cs);
+            }
+            ++n_uses;
+        } else {
+            uint32_t g_after = 0;
+            if (loader) {
+                const uint32_t j1 = start + B + tid, j2 = j1 + B;
+                stage_gather(raw[buf ^ 1], rec, g_nxt, j1 < range.y);           // batch b+1, in flight
+                g_after = j2 < range.y ? __ldg(vals + j2) : 0u;                 // id of batch b+2
+            }
+            cp_async_commit();
+            cp_async_wait<1>();  // this thread's gathers of batch b have landed
+            if (loader) stage_transpose(s, raw[buf], rec, g_cur, start + tid < range.y, cs);
+            g_cur = g_nxt;
+            g_nxt = g_after;
         }
-        cp_async_commit();
-        cp_async_wait<1>();  // this thread's gathers of batch b have landed
-        if (loader) stage_transpose(s, raw[buf], rec, g_cur, start + tid < range.y, cs);
-        g_cur = g_nxt;
-        g_nxt = g_after;
         __syncthreads();  // batch b staged, the list written
         my_act = false;
         if (tid < n_active) {
@@ -319,7 +420,13 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
         bal = __ballot_sync(0xffffffffu, my_act);
         if ((tid & 31) == 0) s_warp[tid >> 5] = __popc(bal);
     }
-    cp_async_wait<0>();
+    if constexpr (TMA) {
+        // a batch issued but never consumed (the pixels saturated): let it land before the CTA
+        // exits (its shared memory is the TMA destination)
+        if (tid == 0 && in_flight) mbar_wait(&s_mbar[n_uses & 1], (n_uses >> 1) & 1u);
+    } else {
+        cp_async_wait<0>();
+    }
     __syncthreads();
     if (inside) {
         const float T = st.T[tid];
@@ -822,19 +929,48 @@ cudaError_t launch_render_stats(void *ws, const Layout &L, int W, int H, unsigne
     return cudaGetLastError();
 }
 
+// The render records as a 2-D tensor (N rows of 12 float32) for TMA gather4: one row per
+// Gaussian, box = 1 row (gather4 moves 4 rows of 48 B).  Encoded on the host per launch (the
+// record array belongs to the caller's workspace); cuTensorMapEncodeTiled through the runtime's
+// driver entry point (no libcuda link).
+static cudaError_t records_tensor_map(const float4 *rec, int n, CUtensorMap *tm) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t gdim[2] = {12, (cuuint64_t)(n > 0 ? n : 1)};
+    const cuuint64_t gstride[1] = {48};
+    const cuuint32_t box[2] = {12, 1};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float4 *>(rec), gdim, gstride, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, float bg1, float bg2, float *out_rgb,
                           float *out_T, uint32_t *out_nc, cudaStream_t st) {
     const ss_layout &P = L.pub;
     if (P.n_tiles == 0) return cudaSuccess;
     const int grid = P.n_tiles * (256 / kRenderPix);
+    CUtensorMap tm;
+    std::memset(&tm, 0, sizeof(tm));
+    if (kRenderTma) {
+        const cudaError_t e = records_tensor_map(at<const float4>(ws, P.rec), L.n, &tm);
+        if (e != cudaSuccess) return e;
+    }
     if (out_nc)
-        launch_pdl(k_render<true, kRenderPix, kRenderBatch>, grid, kRenderPix, 0, st, at<const uint2>(ws, P.ranges),
-                   at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
-                   out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src));
+        launch_pdl(k_render<true, kRenderPix, kRenderBatch, kRenderTma>, grid, kRenderPix, 0, st,
+                   at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec),
+                   W, H, P.tiles_x, bg0, bg1, bg2, out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src), tm);
     else
-        launch_pdl(k_render<false, kRenderPix, kRenderBatch>, grid, kRenderPix, 0, st, at<const uint2>(ws, P.ranges),
-                   at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
-                   out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src));
+        launch_pdl(k_render<false, kRenderPix, kRenderBatch, kRenderTma>, grid, kRenderPix, 0, st,
+                   at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec),
+                   W, H, P.tiles_x, bg0, bg1, bg2, out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src), tm);
     return cudaGetLastError();
 }
 
@@ -860,9 +996,15 @@ cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg
     // forward walk = k_render with T_final / n_contrib (no image), then the back-to-front walk
     float *pT = at<float>(ws, L.pix_T);
     uint32_t *pl = at<uint32_t>(ws, L.pix_last);
-    launch_pdl(k_render<true, kRenderPix, kRenderBatch>, P.n_tiles * (256 / kRenderPix), kRenderPix, 0, st,
-               at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W,
-               H, P.tiles_x, bg0, bg1, bg2, (float *)nullptr, pT, pl, at<const ColorSrc>(ws, L.color_src));
+    CUtensorMap tm;
+    std::memset(&tm, 0, sizeof(tm));
+    if (kRenderTma) {
+        const cudaError_t e = records_tensor_map(at<const float4>(ws, P.rec), L.n, &tm);
+        if (e != cudaSuccess) return e;
+    }
+    launch_pdl(k_render<true, kRenderPix, kRenderBatch, kRenderTma>, P.n_tiles * (256 / kRenderPix), kRenderPix, 0,
+               st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec),
+               W, H, P.tiles_x, bg0, bg1, bg2, (float *)nullptr, pT, pl, at<const ColorSrc>(ws, L.color_src), tm);
     launch_pdl(k_score_bwd, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges),
                at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
                (const float *)pT, (const uint32_t *)pl, score, at<const ColorSrc>(ws, L.color_src));
