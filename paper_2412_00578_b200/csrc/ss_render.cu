@@ -15,6 +15,7 @@
 // uses the pinned chain u = fma(a, dx, (2b) dy); q = fma(dx, u, (c dy) dy) with explicit
 // round-to-nearest intrinsics, so it is bit-identical to the oracle's; alpha uses the SFU
 // exp2 (ex2.approx), which the image tolerance (1e-4) covers.
+#include <cstdlib>
 #include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -40,10 +41,12 @@ constexpr int kRenderUnroll = SS_RENDER_UNROLL;  // pairs per k_render loop iter
 #endif
 constexpr int kRenderPix = SS_RENDER_PIX;      // pixels per k_render CTA (256: a tile, 128: half a tile)
 constexpr int kRenderBatch = SS_RENDER_BATCH;  // Gaussians per k_render batch
-#ifndef SS_RENDER_TMA
-#define SS_RENDER_TMA 0
-#endif
-constexpr bool kRenderTma = SS_RENDER_TMA != 0;  // batch staging by TMA gather4 (else cp.async)
+// Batch staging of k_render: cp.async (default) or TMA gather4 (SS_RENDER_STAGING=tma in the
+// environment, read per launch; both variants are compiled in).
+static bool render_tma() {
+    const char *v = std::getenv("SS_RENDER_STAGING");
+    return v && std::strcmp(v, "tma") == 0;
+}
 
 // Shared-memory batch of gathered records, split by use: the per-warp culling box, the conic
 // (skip test), the colour.
@@ -959,18 +962,23 @@ cudaError_t launch_render(void *ws, const Layout &L, int W, int H, float bg0, fl
     const int grid = P.n_tiles * (256 / kRenderPix);
     CUtensorMap tm;
     std::memset(&tm, 0, sizeof(tm));
-    if (kRenderTma) {
+    const bool tma = render_tma();
+    if (tma) {
         const cudaError_t e = records_tensor_map(at<const float4>(ws, P.rec), L.n, &tm);
         if (e != cudaSuccess) return e;
     }
-    if (out_nc)
-        launch_pdl(k_render<true, kRenderPix, kRenderBatch, kRenderTma>, grid, kRenderPix, 0, st,
-                   at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec),
-                   W, H, P.tiles_x, bg0, bg1, bg2, out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src), tm);
+#define SS_RENDER_ARGS                                                                                           \
+    at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H,    \
+        P.tiles_x, bg0, bg1, bg2, out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src), tm
+    if (out_nc && tma)
+        launch_pdl(k_render<true, kRenderPix, kRenderBatch, true>, grid, kRenderPix, 0, st, SS_RENDER_ARGS);
+    else if (out_nc)
+        launch_pdl(k_render<true, kRenderPix, kRenderBatch, false>, grid, kRenderPix, 0, st, SS_RENDER_ARGS);
+    else if (tma)
+        launch_pdl(k_render<false, kRenderPix, kRenderBatch, true>, grid, kRenderPix, 0, st, SS_RENDER_ARGS);
     else
-        launch_pdl(k_render<false, kRenderPix, kRenderBatch, kRenderTma>, grid, kRenderPix, 0, st,
-                   at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec),
-                   W, H, P.tiles_x, bg0, bg1, bg2, out_rgb, out_T, out_nc, at<const ColorSrc>(ws, L.color_src), tm);
+        launch_pdl(k_render<false, kRenderPix, kRenderBatch, false>, grid, kRenderPix, 0, st, SS_RENDER_ARGS);
+#undef SS_RENDER_ARGS
     return cudaGetLastError();
 }
 
@@ -998,13 +1006,19 @@ cudaError_t launch_prune_score(void *ws, const Layout &L, int W, int H, float bg
     uint32_t *pl = at<uint32_t>(ws, L.pix_last);
     CUtensorMap tm;
     std::memset(&tm, 0, sizeof(tm));
-    if (kRenderTma) {
+    const bool tma = render_tma();
+    if (tma) {
         const cudaError_t e = records_tensor_map(at<const float4>(ws, P.rec), L.n, &tm);
         if (e != cudaSuccess) return e;
     }
-    launch_pdl(k_render<true, kRenderPix, kRenderBatch, kRenderTma>, P.n_tiles * (256 / kRenderPix), kRenderPix, 0,
-               st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec),
-               W, H, P.tiles_x, bg0, bg1, bg2, (float *)nullptr, pT, pl, at<const ColorSrc>(ws, L.color_src), tm);
+    if (tma)
+        launch_pdl(k_render<true, kRenderPix, kRenderBatch, true>, P.n_tiles * (256 / kRenderPix), kRenderPix, 0,
+                   st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec),
+                   W, H, P.tiles_x, bg0, bg1, bg2, (float *)nullptr, pT, pl, at<const ColorSrc>(ws, L.color_src), tm);
+    else
+        launch_pdl(k_render<true, kRenderPix, kRenderBatch, false>, P.n_tiles * (256 / kRenderPix), kRenderPix, 0,
+                   st, at<const uint2>(ws, P.ranges), at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec),
+                   W, H, P.tiles_x, bg0, bg1, bg2, (float *)nullptr, pT, pl, at<const ColorSrc>(ws, L.color_src), tm);
     launch_pdl(k_score_bwd, P.n_tiles, 256, 0, st, at<const uint2>(ws, P.ranges),
                at<const uint32_t>(ws, P.sorted_value), at<const float4>(ws, P.rec), W, H, P.tiles_x, bg0, bg1, bg2,
                (const float *)pT, (const uint32_t *)pl, score, at<const ColorSrc>(ws, L.color_src));
