@@ -72,7 +72,8 @@ __device__ __forceinline__ void project(const float4 &q4, const float4 &s4, floa
 __device__ __forceinline__ void write_records(size_t i, int mode, float x2d, float y2d, float a, float b, float c,
                                               double td, float sigma, const int4 &R, uint32_t count, uint32_t n_ent,
                                               uint32_t n_span, bool span_inline, uint32_t cols,
-                                              float4 *__restrict__ rec, uint4 *__restrict__ erec) {
+                                              const uint32_t *pay, float4 *__restrict__ rec,
+                                              uint4 *__restrict__ erec) {
     // render record (48 B): q0 (x, y, a, b) | q1 (c, t, sigma, 0) | q2 (colour flag, r, g, b);
     // the colour (R13) is left pending (flag 0) and computed by the first render-path
     // kernel that gathers the record (ss_color.cuh)
@@ -99,10 +100,11 @@ __device__ __forceinline__ void write_records(size_t i, int mode, float x2d, flo
                                        : (n_ent <= (uint32_t)kInlineEnt ? kInfoEntInline : 0u)) |
                           (cols ? kInfoCols : 0u) | (mode == SS_BIN_ACCUTILE ? kInfoAccuTile : 0u) |
                           (n_ent << kInfoEntShift);
-    if (info & (kInfoSpanInline | kInfoEntInline))
-        *reinterpret_cast<uint2 *>(erec + 2 * (size_t)i) = make_uint2(count, info);
-    else
-        erec[2 * (size_t)i] = make_uint4(count, info, aux0, aux1);
+    // the whole 32 B sector in two 16 B stores (partial-sector writes would cost a DRAM
+    // read-modify-write); the payload was staged in shared memory (pay, 6 words)
+    const bool inl = (info & (kInfoSpanInline | kInfoEntInline)) != 0;
+    erec[2 * (size_t)i] = make_uint4(count, info, inl ? pay[0] : aux0, inl ? pay[1] : aux1);
+    erec[2 * (size_t)i + 1] = make_uint4(pay[2], pay[3], pay[4], pay[5]);
 }
 
 // ---------------------------------------------------------------- a1 preprocess kernel
@@ -132,7 +134,9 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess64(int n,
     if (blockIdx.x == 0 && threadIdx.x == 0) *cs_out = cs_in;  // the render path's lazy colour source
     __shared__ uint32_t s_hist[kDepthPasses][256];
     __shared__ uint32_t s_vis, s_pairs;
+    __shared__ uint32_t s_pay[kPreThreads][7];  // emission-record payload of each thread's Gaussian (stride 7: no bank conflicts)
     for (int k = threadIdx.x; k < kDepthPasses * 256; k += blockDim.x) (&s_hist[0][0])[k] = 0;
+    for (int k = 0; k < 7; ++k) s_pay[threadIdx.x][k] = 0u;
     if (threadIdx.x == 0) s_vis = s_pairs = 0;
     __syncthreads();
     uint32_t my_vis = 0, my_pairs = 0;
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess64(int n,
         bool tall = false;       // AccuTile with more than kLaneRows lines: the warp-collective phase
         // entries (or line spans) go straight to the emission record (only Gaussians with tiles
         // get one; words past the stored count are stale)
-        uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 2 * (size_t)i) + 2;
+        uint32_t *ent_out = s_pay[threadIdx.x];
         uint32_t *span_out = ent_out;
         uint32_t n_span = 0;
         bool span_inline = false;
@@ -250,7 +254,7 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess64(int n,
             accutile_setup((double)bx, (double)by, (double)ba, (double)bb, (double)bc, bt, cam.tiles_x, cam.tiles_y,
                            w);
             uint32_t pairs = 0, ents = 0;
-            uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 2 * (size_t)gi) + 2;
+            uint32_t *ent_out = s_pay[(threadIdx.x & ~31) + src];  // the owner's payload
             const int last = (w.s1 - 1) >> 2;
             for (int b0 = w.s0 >> 2; b0 <= last; b0 += 32) {
                 const int band = b0 + lane;
@@ -281,9 +285,10 @@ __global__ void __launch_bounds__(kPreThreads, kPreBlocks) k_preprocess64(int n,
                 n_ent = ents;
             }
         }
+        __syncwarp();  // the tall sweeps' entries (written by every lane) visible to their owners
         if (count > 0) {
             write_records((size_t)i, mode, x2d, y2d, a, b, c, td, mo.w, R, count, n_ent, n_span, span_inline, cols,
-                          rec, erec);
+                          s_pay[threadIdx.x], rec, erec);
             const uint32_t key = __float_as_uint(pz);
             depth_key[i] = key;
             gne[i] = n_ent;
@@ -338,7 +343,9 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
     if (blockIdx.x == 0 && threadIdx.x == 0) *cs_out = cs_in;  // the render path's lazy colour source
     __shared__ uint32_t s_hist[kDepthPasses][256];
     __shared__ uint32_t s_vis, s_pairs;
+    __shared__ uint32_t s_pay[kPreThreads][7];  // emission-record payload of each thread's Gaussian (stride 7: no bank conflicts)
     for (int k = threadIdx.x; k < kDepthPasses * 256; k += blockDim.x) (&s_hist[0][0])[k] = 0;
+    for (int k = 0; k < 7; ++k) s_pay[threadIdx.x][k] = 0u;
     if (threadIdx.x == 0) s_vis = s_pairs = 0;
     __syncthreads();
     uint32_t my_vis = 0, my_pairs = 0;
@@ -362,7 +369,7 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
         float x2d = 0.f, y2d = 0.f, a = 0.f, b = 0.f, c = 0.f;
         double td = 0.0;
         int4 R = make_int4(0, 0, 0, 0);
-        uint32_t *ent_out = reinterpret_cast<uint32_t *>(erec + 2 * (size_t)i) + 2;
+        uint32_t *ent_out = s_pay[threadIdx.x];
         if (valid && pz >= cam.z_near) {
             const float4 q4 = rot[i];
             const float4 s4 = scale[i];
@@ -445,7 +452,7 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
                 sweep32_setup(S2, rect32(S2, cam.tiles_x, cam.tiles_y), bx, by, ba, bb, bc, w);
                 uint32_t pairs = 0, ents = 0;
                 bool sure = true;
-                uint32_t *eo = reinterpret_cast<uint32_t *>(erec + 2 * (size_t)gi) + 2;
+                uint32_t *eo = s_pay[(threadIdx.x & ~31) + src];  // the owner's payload
                 const int last = (w.s1 - 1) >> 2;
                 for (int b0 = w.s0 >> 2; b0 <= last; b0 += 32) {
                     const int band = b0 + lane;
@@ -479,6 +486,7 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
                 }
             }
         }
+        __syncwarp();  // the tall sweeps' entries (written by every lane) visible to their owners
         // deferred Gaussians: appended to the float64 path's queue (warp-aggregated)
         const uint32_t dmask = __ballot_sync(0xffffffffu, defer);
         if (dmask) {
@@ -490,7 +498,7 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
         if (defer) continue;
         if (count > 0) {
             write_records((size_t)i, MODE, x2d, y2d, a, b, c, td, mo.w, R, count, n_ent, n_span, span_inline, cols,
-                          rec, erec);
+                          s_pay[threadIdx.x], rec, erec);
             const uint32_t key = __float_as_uint(pz);
             depth_key[i] = key;
             gne[i] = n_ent;
