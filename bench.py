@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--workload", default="mnr360-3m")
     ap.add_argument("--mode", default="accutile", choices=["3sigma", "snugbox", "accutile"])
     ap.add_argument("--views-per-step", type=int, default=64)
-    ap.add_argument("--streams", type=int, default=8, help="concurrent frame workspaces (FramePipeline)")
+    ap.add_argument("--streams", type=int, default=16, help="concurrent frame workspaces (FramePipeline)")
     ap.add_argument("--prune-ratio", type=float, default=0.0,
                     help="pruned-model regime: score all views (a7 + all_reduce), prune this fraction, bench the rest")
     ap.add_argument("--no-e2e", action="store_true")

@@ -18,6 +18,14 @@ scene, cams = synth.make_workload("mnr360-3m")
 ds = DeviceScene.from_host(scene)
 W, H = cams[0].width, cams[0].height
 NS, V = 8, 64
+if "--pruned" in sys.argv:  # BASELINE config 5: U~ over every view, 90% removed
+    from paper_2412_00578_b200.raster import prune
+    sp = FramePipeline(ds, W, H, n_streams=NS)
+    sp.ensure_capacity(cams)
+    sc = torch.zeros(ds.n, dtype=torch.float64, device="cuda")
+    sp.score_views(cams, sc)
+    ds, _ = prune(ds, sc, 0.9)
+    del sp
 pipe = FramePipeline(ds, W, H, n_streams=NS)
 views = [camera_struct(cams[v]) for v in range(0, 185, 3)][:V]
 pipe.ensure_capacity(views)

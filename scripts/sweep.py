@@ -74,7 +74,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--views", type=int, default=64)
-    ap.add_argument("--streams", type=int, default=8)
+    ap.add_argument("--streams", type=int, default=16)
     args = ap.parse_args()
     for name in ["mnr360-3m", "truck", "garden", "playroom"]:
         scene, cams = synth.make_workload(name)
