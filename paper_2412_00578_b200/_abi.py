@@ -7,7 +7,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libss.so")
+LIB_PATH = os.environ.get("SS_LIB_PATH") or os.path.join(HERE, "libss.so")  # SS_LIB_PATH: a variant build
 
 SS_OK, SS_ERR_INVALID_ARG, SS_ERR_CAPACITY, SS_ERR_CUDA, SS_ERR_UNSUPPORTED = range(5)
 MODES = {"3sigma": 0, "snugbox": 1, "accutile": 2}

@@ -14,8 +14,11 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libss.so")
+# SS_BUILD_TAG=<tag> builds a variant (e.g. the fault-injection build) into _build_<tag>/ and
+# libss_<tag>.so, leaving libss.so alone; load it with SS_LIB_PATH (see _abi.py).
+_TAG = os.environ.get("SS_BUILD_TAG", "")
+BUILD = os.path.join(HERE, "_build" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(HERE, f"libss_{_TAG}.so" if _TAG else "libss.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -4,6 +4,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ss_common.cuh"
 
 namespace ss {
@@ -83,6 +85,13 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     P.total_bytes = off;
     return true;
 }
+
+// NVTX range around every enqueueing call (the tracing of SURVEY.md §5): visible to nsys / ncu
+// --nvtx; a no-op when no tool is attached.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local char g_cuda_err[256] = "";
 
@@ -172,6 +181,7 @@ ss_status ss_frame_layout(int32_t n, uint32_t capacity, int32_t width, int32_t h
 
 ss_status ss_preprocess(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
                         void *stream) {
+    NvtxRange nvtx_("ss_preprocess");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -186,6 +196,7 @@ ss_status ss_preprocess(const ss_scene *scene, const ss_camera *cam, ss_bin_mode
 }
 
 ss_status ss_bin(const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame, void *stream) {
+    NvtxRange nvtx_("ss_bin");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -201,6 +212,7 @@ ss_status ss_bin(const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame, 
 }
 
 ss_status ss_sort(const ss_frame *frame, void *stream) {
+    NvtxRange nvtx_("ss_sort");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -208,6 +220,7 @@ ss_status ss_sort(const ss_frame *frame, void *stream) {
 }
 
 ss_status ss_sorted_keys(const ss_frame *frame, uint64_t *keys, void *stream) {
+    NvtxRange nvtx_("ss_sorted_keys");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -217,6 +230,7 @@ ss_status ss_sorted_keys(const ss_frame *frame, uint64_t *keys, void *stream) {
 
 ss_status ss_render(const ss_frame *frame, const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib,
                     void *stream) {
+    NvtxRange nvtx_("ss_render");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -226,6 +240,7 @@ ss_status ss_render(const ss_frame *frame, const float *bg, float *out_rgb, floa
 }
 
 ss_status ss_finalize_colours(const ss_frame *frame, void *stream) {
+    NvtxRange nvtx_("ss_finalize_colours");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -233,6 +248,7 @@ ss_status ss_finalize_colours(const ss_frame *frame, void *stream) {
 }
 
 ss_status ss_render_stats(const ss_frame *frame, uint64_t *counters, void *stream) {
+    NvtxRange nvtx_("ss_render_stats");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -243,6 +259,7 @@ ss_status ss_render_stats(const ss_frame *frame, uint64_t *counters, void *strea
 }
 
 ss_status ss_prune_score(const ss_frame *frame, const float *bg, double *score, void *stream) {
+    NvtxRange nvtx_("ss_prune_score");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -253,6 +270,7 @@ ss_status ss_prune_score(const ss_frame *frame, const float *bg, double *score, 
 
 ss_status ss_render_backward(const ss_frame *frame, const float *bg, const float *dL_dimg, const float *T_final,
                              const uint32_t *n_contrib, float *grad2d, void *stream) {
+    NvtxRange nvtx_("ss_render_backward");
     Layout L;
     ss_status s = check_frame(frame, &L);
     if (s != SS_OK) return s;
@@ -263,6 +281,7 @@ ss_status ss_render_backward(const ss_frame *frame, const float *bg, const float
 
 static ss_status preprocess_backward(const ss_scene *scene, const ss_camera *cam, const float *grad2d,
                                      const ss_scene_grad *grad, uint8_t *flags, void *stream) {
+    NvtxRange nvtx_("ss_preprocess_backward");
     if (!scene || !cam || !grad || scene->n < 0 || scene->sh_degree < 0 || scene->sh_degree > 3) return SS_ERR_INVALID_ARG;
     if (grad->n != scene->n || grad->sh_degree != scene->sh_degree) return SS_ERR_INVALID_ARG;
     if (scene->n >= (1 << 30)) return SS_ERR_UNSUPPORTED;
@@ -294,12 +313,14 @@ static bool grad_ok(const ss_scene_grad *g, int32_t n, int32_t deg) {
 
 ss_status ss_l1_loss_grad(int64_t count, const float *img, const float *gt, float *dL_dimg, double *loss_sum,
                           void *stream) {
+    NvtxRange nvtx_("ss_l1_loss_grad");
     if (count < 0 || (count > 0 && (!img || !gt || !dL_dimg || !loss_sum))) return SS_ERR_INVALID_ARG;
     return cuda_status(launch_l1_loss_grad(count, img, gt, dL_dimg, loss_sum, static_cast<cudaStream_t>(stream)));
 }
 
 ss_status ss_adam_init(const ss_scene *scene, const ss_scene_grad *raw, const ss_scene_grad *m,
                        const ss_scene_grad *v, void *stream) {
+    NvtxRange nvtx_("ss_adam_init");
     if (!scene || scene->n < 0 || scene->sh_degree < 0 || scene->sh_degree > 3) return SS_ERR_INVALID_ARG;
     if (scene->n > 0 && (!scene->mean_opac || !scene->scale || !scene->rot || !scene->sh)) return SS_ERR_INVALID_ARG;
     if (!grad_ok(raw, scene->n, scene->sh_degree) || !grad_ok(m, scene->n, scene->sh_degree) ||
@@ -311,6 +332,7 @@ ss_status ss_adam_init(const ss_scene *scene, const ss_scene_grad *raw, const ss
 static ss_status adam_step(const ss_scene_grad *grad, const ss_scene_grad *raw, const ss_scene_grad *m,
                            const ss_scene_grad *v, const ss_scene_grad *scene, const ss_adam_config *cfg,
                            const uint8_t *flags, void *stream) {
+    NvtxRange nvtx_("ss_adam_step");
     if (!grad || !cfg || grad->n < 0 || grad->sh_degree < 0 || grad->sh_degree > 3) return SS_ERR_INVALID_ARG;
     const int32_t n = grad->n, d = grad->sh_degree;
     if (!grad_ok(grad, n, d) || !grad_ok(raw, n, d) || !grad_ok(m, n, d) || !grad_ok(v, n, d) || !grad_ok(scene, n, d))
@@ -337,6 +359,7 @@ ss_status ss_adam_step_flagged(const ss_scene_grad *grad, const ss_scene_grad *r
 
 ss_status ss_render_frame(const ss_scene *scene, const ss_camera *cam, ss_bin_mode mode, const ss_frame *frame,
                           const float *bg, float *out_rgb, float *out_T, uint32_t *out_ncontrib, void *stream) {
+    NvtxRange nvtx_("ss_render_frame");
     ss_status s = ss_preprocess(scene, cam, mode, frame, stream);
     if (s == SS_OK) s = ss_bin(cam, mode, frame, stream);
     if (s == SS_OK) s = ss_sort(frame, stream);
@@ -356,6 +379,7 @@ uint32_t ss_prune_count(int32_t n, double ratio) {
 
 ss_status ss_prune_select(const double *score, int32_t n, double ratio, uint8_t *keep, void *ws, size_t ws_bytes,
                           void *stream) {
+    NvtxRange nvtx_("ss_prune_select");
     if (n < 0 || !(ratio >= 0.0) || !(ratio <= 1.0)) return SS_ERR_INVALID_ARG;
     if (n >= (1 << 30)) return SS_ERR_UNSUPPORTED;
     if (n > 0 && (!score || !keep)) return SS_ERR_INVALID_ARG;
@@ -365,6 +389,7 @@ ss_status ss_prune_select(const double *score, int32_t n, double ratio, uint8_t 
 
 ss_status ss_compact_scene(const ss_scene *in, const uint8_t *keep, const ss_scene *out, uint32_t *n_out,
                            void *ws, size_t ws_bytes, void *stream) {
+    NvtxRange nvtx_("ss_compact_scene");
     if (!in || !out || !n_out || in->n < 0 || in->sh_degree < 0 || in->sh_degree > 3) return SS_ERR_INVALID_ARG;
     if (out->sh_degree != in->sh_degree || out->n < 0 || out->n > in->n) return SS_ERR_INVALID_ARG;
     if (in->n > 0 && (!keep || !in->mean_opac || !in->scale || !in->rot || !in->sh)) return SS_ERR_INVALID_ARG;

@@ -140,8 +140,13 @@ __device__ __forceinline__ void sweep_line(const Sweep &w, double line, bool com
 __device__ __forceinline__ void sweep_row(const Sweep &w, int r, double imin_lo, double imin_hi, double imax_lo,
                                           double imax_hi, int &tmin, int &tmax) {
     const double lo_r = (double)(r * kTile), hi_r = (double)((r + 1) * kTile);
+#ifdef SS_FAULT_SKIP_TANGENT_ROW  // fault-injection build: the tangent-point row test dropped
+    const double e_min = imin_lo < imax_lo ? imin_lo : imax_lo;
+    const double e_max = imin_hi > imax_hi ? imin_hi : imax_hi;
+#else
     const double e_min = (w.tmin_s >= lo_r && w.tmin_s < hi_r) ? w.ext_lo : (imin_lo < imax_lo ? imin_lo : imax_lo);
     const double e_max = (w.tmax_s >= lo_r && w.tmax_s < hi_r) ? w.ext_hi : (imin_hi > imax_hi ? imin_hi : imax_hi);
+#endif
     double g0 = floor(e_min / kTile), g1 = floor(e_max / kTile) + 1.0;
     if (!(g0 > w.f0)) g0 = w.f0;
     if (g0 > w.f1) g0 = w.f1;

@@ -172,8 +172,13 @@ __device__ __forceinline__ bool line32(const Sweep32 &w, int j, bool first, int 
 // Row r from its boundary lines' floors: [tmin, tmax) of Algorithm 1 (sweep_row).
 __device__ __forceinline__ void row32(const Sweep32 &w, int r, int klo0, int khi0, int klo1, int khi1, int &tmin,
                                       int &tmax) {
+#ifdef SS_FAULT_SKIP_TANGENT_ROW  // fault-injection build: the tangent-point row test dropped
+    const int g0 = min(klo0, klo1);
+    const int g1 = max(khi0, khi1) + 1;
+#else
     const int g0 = w.k_tmin == r ? w.k_ext_lo : min(klo0, klo1);
     const int g1 = (w.k_tmax == r ? w.k_ext_hi : max(khi0, khi1)) + 1;
+#endif
     tmin = g0 <= w.f0 ? w.f0 : (g0 > w.f1 ? w.f1 : g0);
     tmax = g1 <= w.f0 ? w.f0 : (g1 > w.f1 ? w.f1 : g1);
 }
