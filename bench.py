@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="enqueue every frame's kernels instead of one CUDA graph")
     ap.add_argument("--no-pruned", action="store_true", help="skip the pruned-regime (config 5) measurement")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs (truck, garden, playroom)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-score", action="store_true")
     ap.add_argument("--no-backward", action="store_true")
@@ -623,6 +624,16 @@ def run_ours(args):
                                "between steps"}
         del ppipe, pds
 
+    # ---- the other BASELINE.json configs, same launch setup (view-sharded over the ranks, graphs,
+    # frames in flight, L2 flushed between steps), fewer steps: truck-shaped in the three tile
+    # modes (config 2), garden-shaped (config 3), playroom-shaped with the score pass and its
+    # all_reduce over every view (config 4), and each scene pruned by 90% (config 5)
+    configs_info = None
+    if not args.no_configs and not args.ncu and prune_info is None:
+        del pipe
+        torch.cuda.empty_cache()
+        configs_info = run_configs(args, rank, world, dev, stream, flush)
+
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.ncu:
@@ -681,6 +692,7 @@ def run_ours(args):
             "backward": bw_info,
             "train": train_info,
             "pruned": pruned_info,
+            "configs": configs_info,
             "cpu_baseline": cpu,
             "paper_context": {"gpu": "RTX A5000 (PAPER.md P:447)", "accutile_fps_avg_scene": 267,
                               "speedups": {"snugbox": 1.82, "accutile": 1.99, "overall": 6.71}},
@@ -703,6 +715,87 @@ def spawn_ranks(n: int) -> int:
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
     return subprocess.call(cmd, env=env)
+
+
+def run_configs(args, rank, world, dev, stream, flush, V=64, steps=3, warmup=2):
+    """Frames/s of the other BASELINE configs (see the caller)."""
+    import torch
+
+    from paper_2412_00578_b200 import dist, synth
+    from paper_2412_00578_b200.raster import DeviceScene, FramePipeline, camera_struct, prune
+
+    def fps(ds, cams, mode):
+        W, H = cams[0].width, cams[0].height
+        mine = dist.views_for_rank(len(cams), rank, world)
+        cs = [camera_struct(cams[v]) for v in mine]
+        pipe = FramePipeline(ds, W, H, mode=mode, n_streams=args.streams)
+        P = pipe.ensure_capacity(cs)
+        pipe.render_views(cs[:args.streams])
+        pipe.capture(cs)
+        seq = [cs[j % len(cs)] for j in range((warmup + steps) * V)]
+        for j in range(warmup):
+            pipe.render_views(seq[j * V:(j + 1) * V], graphs=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        ms = 0.0
+        for k in range(steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            pipe.render_views(seq[(warmup + k) * V:(warmup + k + 1) * V], graphs=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ms += a.elapsed_time(b)
+        assert pipe.overflow_count() == 0
+        ms = dist.max_over_ranks(ms)
+        return {"fps": world * steps * V / (ms / 1e3), "max_pairs_per_frame": P}, pipe, cs
+
+    def score_all(ds, cams, pipe, cs, bg=(0.0, 0.0, 0.0)):
+        score = torch.zeros(ds.n, dtype=torch.float64, device=dev)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        a.record(stream)
+        pipe.score_views(cs, score, bg)
+        b.record(stream)
+        dist.allreduce_scores(score)
+        c.record(stream)
+        torch.cuda.synchronize()
+        pipe.check_overflow()
+        info = {"views": len(cams), "views_per_s": len(cams) / (dist.max_over_ranks(a.elapsed_time(b)) / 1e3),
+                "allreduce": {"ms": dist.max_over_ranks(b.elapsed_time(c)), "bytes": 8 * ds.n,
+                              "backend": dist.backend()} if world > 1 else "skipped (world 1)"}
+        return score, info
+
+    out = {}
+    for name, modes in (("truck", ("3sigma", "snugbox", "accutile")), ("garden", ("snugbox", "accutile")),
+                        ("playroom", ("accutile",))):
+        scene, cams = synth.make_workload(name)
+        ds = DeviceScene.from_host(scene, dev)
+        res = {"n_gaussians": scene.n, "width": cams[0].width, "height": cams[0].height, "views": len(cams)}
+        pipe = cs = None
+        for mode in modes:
+            del pipe
+            r, pipe, cs = fps(ds, cams, mode)
+            res[mode] = r
+        if "3sigma" in res:
+            res["speedup_vs_3sigma"] = {m: res[m]["fps"] / res["3sigma"]["fps"] for m in modes}
+        # every view's U~ (this rank's shard, then the all_reduce), then the prune step (90%)
+        score, sinfo = score_all(ds, cams, pipe, cs)
+        if name == "playroom":
+            res["score_pass"] = sinfo
+        del pipe
+        pds, _ = prune(ds, score, 0.9)
+        del score
+        r, pipe, _ = fps(pds, cams, "accutile")
+        res["pruned0.9"] = {**r, "n_gaussians": pds.n, "speedup_vs_accutile": r["fps"] / res["accutile"]["fps"]}
+        del pipe, pds, ds, scene
+        torch.cuda.empty_cache()
+        out[name] = res
+    out["note"] = (f"{V} views per step, {steps} timed steps after {warmup}, {args.streams} frames in flight, one CUDA "
+                   "graph per frame, L2 flushed between steps; pruned = U~ over every view (sharded, all_reduce), "
+                   "then the prune step removing 90%")
+    return out
 
 
 def main():
