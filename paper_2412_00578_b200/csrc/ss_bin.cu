@@ -25,7 +25,10 @@
 
 namespace ss {
 
-constexpr int kEntriesCtasPerSm = 8;  // k_entries grid (grid-stride over the visible Gaussians)
+#ifndef SS_ENTRIES_CTAS
+#define SS_ENTRIES_CTAS 8
+#endif
+constexpr int kEntriesCtasPerSm = SS_ENTRIES_CTAS;  // k_entries grid (grid-stride over the visible Gaussians)
 namespace {
 
 constexpr int kScanThreads = 256;

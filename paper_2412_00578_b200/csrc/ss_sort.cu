@@ -22,7 +22,7 @@ constexpr int kLB = SS_SORT_LB;  // look-back predecessors read per round trip
 #endif
 constexpr int kLBSleepNs = SS_SORT_SLEEP;
 #ifndef SS_SORT_GRID
-#define SS_SORT_GRID 4  // persistent onesweep CTAs per SM
+#define SS_SORT_GRID 2  // persistent onesweep CTAs per SM (16 frames in flight: 2 -> 1945 fps, 3 -> 1931, 4 -> 1924)
 #endif
 #ifndef SS_SORT_MATCH
 #define SS_SORT_MATCH 1
