@@ -168,6 +168,35 @@ def tiny_scene(n=1000, seed=0, low_sigma=False, sh_degree=3) -> tuple[Scene, Cam
     return scene, cam
 
 
+def knife_scene(n=20000, seed=11, sh_degree=0) -> tuple[Scene, Camera]:
+    """Stress scene for the tile decisions (the float32-certified geometry of ss_preprocess and
+    its float64 fallback): the tiny camera; means on or within 1e-5..1e-1 px of tile lines and
+    tile corners, extreme anisotropy (axis ratios up to 1e3, Haar rotations: thin, strongly
+    correlated conics), opacities from just above 1/255 (t ~ 0: tiny ellipses) to 0.999,
+    footprints from sub-pixel to several hundred pixels (clipped at the image border)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    W = H = 256
+    cam = look_at((0, 0, 0), (0, 0, 1), W, H, 60.0, up=(0, -1, 0))
+    fx = cam.fx
+    line = lambda m: 16.0 * rng.integers(-2, 19, m)
+    off = lambda m: rng.choice([0.0, 1e-5, -1e-5, 1e-3, -1e-3, 0.1, -0.1], m) * rng.uniform(0.5, 1.5, m)
+    u = np.where(rng.uniform(size=n) < 0.7, line(n) + off(n), rng.uniform(-32, W + 32, n))
+    v = np.where(rng.uniform(size=n) < 0.7, line(n) + off(n), rng.uniform(-32, H + 32, n))
+    z = rng.uniform(1.0, 10.0, n)
+    x = (u - cam.cx) * z / fx
+    y = (v - cam.cy) * z / fx
+    big = np.exp(rng.uniform(math.log(0.3), math.log(200.0), n))          # px, the long axis
+    ratio = np.exp(rng.uniform(0.0, math.log(1e3), (n, 2)))
+    px = np.stack([big, big / ratio[:, 0], big / ratio[:, 1]], 1)
+    scale = px * z[:, None] / fx
+    opac = np.where(rng.uniform(size=n) < 0.3, 1.0 / 255.0 + rng.uniform(1e-7, 1e-3, n),
+                    rng.uniform(0.05, 0.999, n))
+    mean_opac = np.stack([x, y, z, opac], 1).astype(np.float32)
+    sc = np.concatenate([scale, np.zeros((n, 1))], 1).astype(np.float32)
+    scene = Scene(mean_opac, sc, _haar_quaternions(rng, n), _sh_planes(rng, n, sh_degree), sh_degree, "knife")
+    return scene, cam
+
+
 def dense_scene(n=12000, seed=5, tie_frac=0.5, sh_degree=1) -> tuple[Scene, Camera]:
     """Tile-sort stress case on the tiny camera: means packed into a 64x64 px window at the
     image centre, so the central tiles' lists are longer than one shared-memory sort

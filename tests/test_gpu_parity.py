@@ -202,3 +202,25 @@ def test_phantom_pairs_invariant(name):
     (ps, fs), (pa, fa) = res["snugbox"], res["accutile"]
     assert 0 <= fa <= fs and fa < pa
     assert ps - fs == pa - fa, res
+
+
+@pytest.mark.parametrize("mode", ["snugbox", "accutile"])
+@pytest.mark.parametrize("seed", [11, 12, 13])
+def test_knife_edge_tile_decisions(mode, seed):
+    """synth.knife_scene: means on / within 1e-5 px of tile lines, axis ratios up to 1e3,
+    t ~ 0 and near-1 opacities, clipped giants.  Every count, sorted key and range equals the
+    oracle's float64 tile sets bit-exactly; the float32-certified path must have handed some
+    Gaussians to the float64 fallback here (pre_deferred > 0), so both paths are exercised."""
+    from paper_2412_00578_b200.raster import DeviceScene, Rasterizer
+    scene, cam = synth.knife_scene(seed=seed)
+    rz = Rasterizer(DeviceScene.from_host(scene), cam.width, cam.height, mode=mode)
+    rz.ensure_capacity(cam)
+    rz.render_frame(cam)
+    torch.cuda.synchronize()
+    t = rz.totals()
+    f = oracle.frame(scene, cam, mode, render=False, cap_hint=t["pairs"] + 16)
+    assert np.array_equal(rz.counts().cpu().numpy().view(np.uint32), f.counts)
+    assert t["pairs"] == f.P
+    assert np.array_equal(rz.sorted_keys().cpu().numpy().view(np.uint64)[:f.P], f.keys)
+    assert np.array_equal(rz.ranges().cpu().numpy().view(np.uint32), f.ranges)
+    assert t["deferred"] > 0, "the float64 fallback was not exercised"
