@@ -46,11 +46,14 @@ __device__ __forceinline__ float rsqrt_a(float x) {
 
 // floor(v / 16) certified for every value within e of v (the float64 value among them):
 // returns false if [v - e, v + e] touches a tile line.  k is clamped to [-kBig, kBig].
+// d = v - 16 f is exact (v / 16 is exact, f = floor(v / 16), and d in [0, 16) is a multiple of
+// ulp(v) when ulp(v) <= 16; for |v| >= 2^28, d = 0 and the test fails), so the interval lies
+// strictly inside (16 f, 16 f + 16) iff e < d < 16 - e; 16 - e is rounded down.
 __device__ __forceinline__ bool floor16(float v, float e, int &k) {
     const float f = floorf(__fmul_rn(v, 0.0625f));
-    const float lo = __fmul_rn(f, 16.0f);
+    const float d = __fmaf_rn(f, -16.0f, v);
     k = (int)fminf(fmaxf(f, -(float)kBig), (float)kBig);
-    return __fsub_rn(v, lo) > e && __fsub_rn(__fadd_rn(lo, 16.0f), v) > e;
+    return d > e && d < __fsub_rd(16.0f, e);
 }
 
 enum { kSure = 0, kCull = 1, kUnsure = 2 };
@@ -72,8 +75,9 @@ __device__ __forceinline__ int snug32(float mx, float my, float a, float b, floa
     const float eD = 1.5f * kU * (fabsf(ac) + bb + fabsf(D));
     if (D <= -eD) return kCull;
     if (!(D > 8.0f * eD)) return kUnsure;  // the sign of D, or its relative accuracy, is not certain
-    const float relD = eD / D;
     const float rD = rcp_a(D);                                       // rel relD + 4u
+    // relD = eD / D bounded from above: rD has relative error <= 4u, the product u
+    const float relD = __fmul_rn(__fmul_rn(eD, rD), 1.0001f);
     const float hx = sqrt_a(__fmul_rn(__fmul_rn(t, c), rD));         // rel relD / 2 + 7.5u
     const float hy = sqrt_a(__fmul_rn(__fmul_rn(t, a), rD));
     const float rel_h = (0.5f * relD + 8.0f * kU) * 1.25f;
@@ -82,22 +86,26 @@ __device__ __forceinline__ int snug32(float mx, float my, float a, float b, floa
     s.D = D;
     s.relD = relD;
     s.t = t;
-    const float ehx = hx * rel_h, ehy = hy * rel_h;
-    bool ok = true;
-    auto fl = [&](float v, float e, int &k) { ok &= floor16(v, (e + kU * fabsf(v)) * 1.1f + 1e-30f, k); };
-    fl(__fsub_rn(mx, hx), ehx, s.kx0);
-    fl(__fadd_rn(mx, hx), ehx, s.kx1);
-    fl(__fsub_rn(my, hy), ehy, s.ky0);
-    fl(__fadd_rn(my, hy), ehy, s.ky1);
+    // one bound per pair m +- h of values: the value's own rounding u |m +- h| <= u (|m| + |h|)
+    // (error-bound arithmetic only: fused, the 1.1 safety factor covers its rounding)
+    auto pair_bound = [](float m, float h, float eh) {
+        return __fmaf_rn(__fmaf_rn(kU, fabsf(m) + fabsf(h), eh), 1.1f, 1e-30f);
+    };
+    const float ex = pair_bound(mx, hx, hx * rel_h), ey = pair_bound(my, hy, hy * rel_h);
+    bool ok = floor16(__fsub_rn(mx, hx), ex, s.kx0);
+    ok &= floor16(__fadd_rn(mx, hx), ex, s.kx1);
+    ok &= floor16(__fsub_rn(my, hy), ey, s.ky0);
+    ok &= floor16(__fadd_rn(my, hy), ey, s.ky1);
     if (!TANGENTS) return ok ? kSure : kUnsure;
     // tangent points: yl/yr = my +- (b hx) / c, xt/xb = mx +- (b hy) / a; (b h) ic has relative
     // error rel_h + 6u
     const float Tx = __fmul_rn(__fmul_rn(b, hx), s.ic), Ty = __fmul_rn(__fmul_rn(b, hy), s.ia);
-    const float eTx = fabsf(Tx) * (rel_h + 6.0f * kU) * 1.1f, eTy = fabsf(Ty) * (rel_h + 6.0f * kU) * 1.1f;
-    fl(__fadd_rn(my, Tx), eTx, s.kyl);
-    fl(__fsub_rn(my, Tx), eTx, s.kyr);
-    fl(__fadd_rn(mx, Ty), eTy, s.kxt);
-    fl(__fsub_rn(mx, Ty), eTy, s.kxb);
+    const float relT = (rel_h + 6.0f * kU) * 1.1f;
+    const float eTx = pair_bound(my, Tx, fabsf(Tx) * relT), eTy = pair_bound(mx, Ty, fabsf(Ty) * relT);
+    ok &= floor16(__fadd_rn(my, Tx), eTx, s.kyl);
+    ok &= floor16(__fsub_rn(my, Tx), eTx, s.kyr);
+    ok &= floor16(__fadd_rn(mx, Ty), eTy, s.kxt);
+    ok &= floor16(__fsub_rn(mx, Ty), eTy, s.kxb);
     return ok ? kSure : kUnsure;
 }
 
@@ -112,6 +120,7 @@ __device__ __forceinline__ int4 rect32(const Snug32 &s, int tiles_x, int tiles_y
 struct Sweep32 {
     bool rows;
     float mf, ms, af, b, iaf, D, relD, taf;
+    float cD4, ct4, umf;  // per-sweep constants of line32's error bounds
     int s0, s1, f0, f1;
     int k_ext_lo, k_ext_hi;  // floors of the free-axis bbox extremes
     int k_smin, k_smax;      // floors of the swept-axis bbox extremes
@@ -136,6 +145,9 @@ __device__ __forceinline__ void sweep32_setup(const Snug32 &S, const int4 &R, fl
         w.s0 = R.x; w.s1 = R.y; w.f0 = R.z; w.f1 = R.w;
     }
     w.taf = __fmul_rn(S.t, w.af);
+    w.cD4 = (w.relD + 4.0f * kU) * 4.8f;
+    w.ct4 = (fabsf(w.taf) * (2.4f * kU) + 1e-30f) * 4.0f;
+    w.umf = kU * fabsf(w.mf);
 }
 
 // Line j of the sweep: certified floors (klo, khi) of its Eq. 15 intersections, or the neutral
@@ -151,22 +163,34 @@ __device__ __forceinline__ bool line32(const Sweep32 &w, int j, bool first, int 
     const float v = __fsub_rn((float)(j * kTile), w.ms);          // rel u
     const float Dvv = __fmul_rn(w.D, __fmul_rn(v, v));            // rel relD + 4u
     const float disc = __fsub_rn(w.taf, Dvv);                     // taf: rel 2u
-    const float edisc = (fabsf(Dvv) * (w.relD + 4.0f * kU) + fabsf(w.taf) * 2.0f * kU + kU * fabsf(disc)) * 1.2f +
-                        1e-30f;
-    const float d0 = fmaxf(disc, 0.0f);
-    const float s = sqrt_a(d0);
-    // |sqrt(x) - sqrt(y)| <= |x - y| / (2 sqrt(min(x, y))), and <= sqrt(|x - y|) near 0
-    const float es = (disc > 2.0f * edisc ? 0.5f * edisc * rsqrt_a(disc - edisc) : sqrt_a(d0 + edisc)) * 1.1f +
-                     kUa * s;
+    // 4 x the bound on |disc - disc_64|: (|Dvv| (relD + 4u) + |taf| 2u + u |disc|) 1.2 + 1e-30
+    // (bound arithmetic fused; the per-sweep constants are w.cD4 = 4.8 (relD + 4u) and
+    // w.ct4 = 4 (2.4u |taf| + 1e-30))
+    const float edisc4 = __fmaf_rn(fabsf(Dvv), w.cD4, __fmaf_rn(fabsf(disc), 4.8f * kU, w.ct4));
+    // a line within 4 bounds of tangency (disc near 0: the line grazes the bbox extreme) is left
+    // to the float64 path; otherwise, with y the float64 disc, |y - disc| <= e <= disc / 4 and
+    // |sqrt(disc) - sqrt(y)| = |disc - y| / (sqrt(disc) + sqrt(y)) <= e / (1.866 sqrt(disc))
+    //                       <= 0.536 e rsqrt(disc)
+    // s = disc rsqrt(disc) is within 6u of sqrt(disc) (rsqrt: 4u, the product: u)
+    if (!(disc >= edisc4)) return false;
+    const float r = rsqrt_a(disc);
+    const float s = __fmul_rn(disc, r);
+    const float es = __fmaf_rn(__fmul_rn(edisc4, 0.25f * 0.536f * 1.1f), r, s * (6.6f * kU));
     const float bv = __fmul_rn(w.b, v);
     const float nlo = __fsub_rn(-bv, s), nhi = __fadd_rn(-bv, s);
-    const float ebv = fabsf(bv) * 2.1f * kU;
     const float tlo = __fmul_rn(nlo, w.iaf), thi = __fmul_rn(nhi, w.iaf);  // iaf: rel 4u
     const float lo = __fadd_rn(w.mf, tlo), hi = __fadd_rn(w.mf, thi);
+    // one bound for both intersections, with |nlo|, |nhi| <= nmag = |bv| + s, |tlo|, |thi| <=
+    // aia nmag (1 + u), |lo|, |hi| <= |mf| + aia nmag (1 + u):
+    //   (aia (ebv + es + u nmag) + 5.5u aia nmag + u (|mf| + aia nmag)) 1.2 + 1e-30,
+    // ebv = 2.1u |bv|; the (1 + u) factors are inside the 1.2 safety factor
     const float aia = fabsf(w.iaf);
-    const float elo = (aia * (ebv + es + kU * fabsf(nlo)) + fabsf(tlo) * 5.5f * kU + kU * fabsf(lo)) * 1.2f + 1e-30f;
-    const float ehi = (aia * (ebv + es + kU * fabsf(nhi)) + fabsf(thi) * 5.5f * kU + kU * fabsf(hi)) * 1.2f + 1e-30f;
-    return floor16(lo, elo, klo) & floor16(hi, ehi, khi);
+    const float nmag = fabsf(bv) + s;
+    const float tmag = aia * nmag;
+    const float A = __fmaf_rn(kU, nmag, __fmaf_rn(fabsf(bv), 2.1f * kU, es));
+    const float B = __fmaf_rn(tmag, 6.5f * kU, w.umf);  // w.umf = u |mf|
+    const float e = __fmaf_rn(__fmaf_rn(aia, A, B), 1.2f, 1e-30f);
+    return floor16(lo, e, klo) & floor16(hi, e, khi);
 }
 
 // Row r from its boundary lines' floors: [tmin, tmax) of Algorithm 1 (sweep_row).

@@ -57,8 +57,10 @@ def views_for_rank(n_views: int, rank: int, world_size: int) -> list[int]:
 
 
 def allreduce_scores(score: torch.Tensor) -> torch.Tensor:
-    """Sum the per-rank float64 score vectors in place (the one collective of the path)."""
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+    """Sum the per-rank float64 score vectors in place (the one collective of the path).
+    Runs whenever a process group exists (at world size 1 too: the collective is then a copy,
+    but the NCCL path is the one that executes); without one it is a no-op."""
+    if dist.is_available() and dist.is_initialized():
         dist.all_reduce(score, op=dist.ReduceOp.SUM)
     return score
 

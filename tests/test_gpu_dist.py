@@ -82,3 +82,33 @@ def test_two_ranks_one_gpu_gloo(tmp_path):
             pipe.render_views([cams[int(k)]], BG)
             torch.cuda.synchronize()
             assert np.array_equal(got[k], pipe.outs[0].cpu().numpy()), f"view {k} differs on rank {r}"
+
+
+def _nccl_worker(rank, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+    import torch.distributed as tdist
+    from paper_2412_00578_b200 import dist
+    torch.cuda.set_device(0)
+    tdist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    assert dist.backend() == "nccl"
+    ds, cams, pipe = _setup()
+    score = torch.zeros(ds.n, dtype=torch.float64, device="cuda:0")
+    pipe.score_views(cams, score, BG)
+    torch.cuda.synchronize()
+    before = score.clone()
+    dist.allreduce_scores(score)  # NCCL all_reduce(SUM) over the one rank, on the GPU tensor
+    torch.cuda.synchronize()
+    np.save(os.path.join(outdir, "before.npy"), before.cpu().numpy())
+    np.save(os.path.join(outdir, "after.npy"), score.cpu().numpy())
+    tdist.destroy_process_group()
+
+
+def test_nccl_allreduce_one_rank(tmp_path):
+    """The score all_reduce through NCCL (the backend bench.py uses when every rank has its own
+    GPU), on the one GPU these boxes have: world size 1, the libss score vector reduced in place
+    on cuda:0; a one-rank SUM must return the vector unchanged."""
+    import torch.multiprocessing as mp
+    mp.start_processes(_nccl_worker, args=(_free_port(), str(tmp_path)), nprocs=1, join=True, start_method="spawn")
+    before, after = np.load(tmp_path / "before.npy"), np.load(tmp_path / "after.npy")
+    assert (before > 0).sum() > 1000
+    assert np.array_equal(before, after)
