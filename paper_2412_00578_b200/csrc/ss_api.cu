@@ -74,6 +74,7 @@ bool compute_layout(int32_t n, uint32_t capacity, int32_t width, int32_t height,
     P.total_pairs = take(4);
     L->hist_depth = take(4 * 256 * kDepthPasses);
     L->pre_queue_n = take(4);
+    L->pre_ticket = take(4);
     L->zero_pre_end = off;
     L->pre_queue = L->dkA;
     P.pre_deferred = L->pre_queue_n;

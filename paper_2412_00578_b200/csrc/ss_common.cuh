@@ -72,6 +72,7 @@ struct Layout {
     size_t hist_depth;              // uint32 [4][256]
     size_t pre_queue;               // uint32 [n] ss_preprocess's float64 queue (aliases dkA: free until ss_bin)
     size_t pre_queue_n;             // uint32 [1] its length (zeroed with the preprocess region)
+    size_t pre_ticket;              // uint32 [1] k_preprocess32's work ticket (zeroed with it)
     size_t counters;                // uint32 [16] tickets: depth passes, scans, last-CTA counters
     size_t lb_depth;                // uint32 [4][nblk_depth][256]
     size_t lb_escan;                // uint32 [nblk_escan] tile sums of the entry scan

@@ -337,8 +337,8 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
                                                     uint32_t *__restrict__ depth_key, uint32_t *__restrict__ gne,
                                                     uint32_t *__restrict__ hist, uint32_t *__restrict__ n_visible,
                                                     uint32_t *__restrict__ total_pairs, uint32_t *__restrict__ queue,
-                                                    uint32_t *__restrict__ queue_n, ColorSrc cs_in,
-                                                    ColorSrc *__restrict__ cs_out) {
+                                                    uint32_t *__restrict__ queue_n, uint32_t *__restrict__ ticket,
+                                                    ColorSrc cs_in, ColorSrc *__restrict__ cs_out) {
     pdl_enter();
     if (blockIdx.x == 0 && threadIdx.x == 0) *cs_out = cs_in;  // the render path's lazy colour source
     __shared__ uint32_t s_hist[kDepthPasses][256];
@@ -353,13 +353,23 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
     const float limy = cam.clip * ((0.5f * (float)cam.H) / cam.fy);
     const int stx = (cam.tiles_x + kSuper - 1) / kSuper;
     const int lane = threadIdx.x & 31;
-    const int stride = gridDim.x * blockDim.x;
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    // warp chunks of 32 Gaussians: the first one static (global warp id), then tickets (the
+    // next chunk fetched one step ahead, with its mean), so that the warps of the persistent
+    // grid finish together (grid-stride: 0.157 ms single-stream, tickets: 0.144 ms)
+    const int nwarps_all = (gridDim.x * blockDim.x) >> 5;
+    int c_next = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int i = c_next * 32 + lane;
     float4 mo_next = i < n ? mean_opac[i] : make_float4(0.f, 0.f, -1.f, 0.f);
-    for (int i0 = blockIdx.x * blockDim.x + (threadIdx.x & ~31); i0 < n; i0 += stride, i += stride) {
+    for (int i0 = c_next * 32; i0 < n; i0 = c_next * 32, i = i0 + lane) {
+        {
+            uint32_t t = 0;
+            if (lane == 0) t = atomicAdd(ticket, 1u);
+            c_next = nwarps_all + (int)__shfl_sync(0xffffffffu, t, 0);
+        }
         const bool valid = i < n;
         const float4 mo = mo_next;
-        mo_next = i + stride < n ? mean_opac[i + stride] : make_float4(0.f, 0.f, -1.f, 0.f);
+        const int in = c_next * 32 + lane;
+        mo_next = in < n ? mean_opac[in] : make_float4(0.f, 0.f, -1.f, 0.f);
         const float px = cam.V[0] * mo.x + cam.V[1] * mo.y + cam.V[2] * mo.z + cam.V[3];
         const float py = cam.V[4] * mo.x + cam.V[5] * mo.y + cam.V[6] * mo.z + cam.V[7];
         const float pz = cam.V[8] * mo.x + cam.V[9] * mo.y + cam.V[10] * mo.z + cam.V[11];
@@ -569,12 +579,12 @@ cudaError_t launch_preprocess(const ss_scene &sc, const CamArgs &cam, int mode, 
         launch_pdl(k_preprocess32<SS_BIN_ACCUTILE>, grid, kPreThreads, 0, st, sc.n, mo, scl, rot, cam,
                    at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key), at<uint32_t>(ws, L.gne),
                    at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs),
-                   queue, queue_n, csrc, at<ColorSrc>(ws, L.color_src));
+                   queue, queue_n, at<uint32_t>(ws, L.pre_ticket), csrc, at<ColorSrc>(ws, L.color_src));
     else
         launch_pdl(k_preprocess32<SS_BIN_SNUGBOX>, grid, kPreThreads, 0, st, sc.n, mo, scl, rot, cam,
                    at<float4>(ws, P.rec), at<uint4>(ws, P.erec), at<uint32_t>(ws, P.depth_key), at<uint32_t>(ws, L.gne),
                    at<uint32_t>(ws, L.hist_depth), at<uint32_t>(ws, P.n_visible), at<uint32_t>(ws, P.total_pairs),
-                   queue, queue_n, csrc, at<ColorSrc>(ws, L.color_src));
+                   queue, queue_n, at<uint32_t>(ws, L.pre_ticket), csrc, at<ColorSrc>(ws, L.color_src));
     // the deferred Gaussians on the float64 path (a few CTAs; the queue length is on the device)
     launch_pdl(k_preprocess64, sms * kPreBlocks, kPreThreads, 0, st, SS_PRE64_ARGS(queue, queue_n));
     if (e != cudaSuccess) return e;

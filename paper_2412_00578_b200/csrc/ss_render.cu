@@ -94,6 +94,12 @@ __device__ __forceinline__ void tile_pixel(int tile, int tiles_x, int p, int &px
     px = (tile % tiles_x) * kTile + (p & 15);
     py = (tile / tiles_x) * kTile + (p >> 4);
 }
+// The same from the tile's first pixel (tx0, ty0) (tile_pixel of pixel 0): no division in
+// the per-batch loops.
+__device__ __forceinline__ void tile_pixel_at(int tx0, int ty0, int p, int &px, int &py) {
+    px = tx0 + (p & 15);
+    py = ty0 + (p >> 4);
+}
 
 // Per-pixel state kept in shared memory between batches, so that before every batch the
 // still-active pixels can be compacted onto the lowest threads: warps whose pixels have all
@@ -257,6 +263,8 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
     const int tid = threadIdx.x;
     int mpx, mpy;
     tile_pixel(tile, tiles_x, p0 + tid, mpx, mpy);
+    int tx0, ty0;
+    tile_pixel(tile, tiles_x, 0, tx0, ty0);
     const bool inside = mpx < W && mpy < H;
     const uint2 range = ranges[tile];
     st.T[tid] = 1.0f;
@@ -359,7 +367,7 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
         if (tid < n_active) {
             const int pp = st.list[tid];
             int px, py;
-            tile_pixel(tile, tiles_x, p0 + pp, px, py);
+            tile_pixel_at(tx0, ty0, p0 + pp, px, py);
             const float2 FX = f2((float)px), FY = f2((float)py);
             float T = st.T[pp], C0 = st.C0[pp], C1 = st.C1[pp], C2 = st.C2[pp];
             uint32_t last = st.last[pp];
@@ -476,6 +484,8 @@ __global__ void __launch_bounds__(256, 5) k_score_bwd(const uint2 *__restrict__ 
     const int lane = tid & 31, warp = tid >> 5;
     int mpx, mpy;
     tile_pixel(tile, tiles_x, tid, mpx, mpy);
+    int tx0, ty0;
+    tile_pixel(tile, tiles_x, 0, tx0, ty0);
     const bool inside = mpx < W && mpy < H;
     const uint2 range = ranges[tile];
     if (tid == 0) s_max = 0;
@@ -531,7 +541,7 @@ __global__ void __launch_bounds__(256, 5) k_score_bwd(const uint2 *__restrict__ 
             const bool act = tid < n_active;
             const int pp = act ? st.list[tid] : 0;
             int px, py;
-            tile_pixel(tile, tiles_x, pp, px, py);
+            tile_pixel_at(tx0, ty0, pp, px, py);
             const float2 FX = f2((float)px), FY = f2((float)py);
             const uint32_t plast = act ? st.last[pp] : 0u;
             const float Tfin = s_Tfin[pp];
@@ -663,6 +673,8 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
     const int tile = blockIdx.x;
     int mpx, mpy;
     tile_pixel(tile, tiles_x, threadIdx.x, mpx, mpy);
+    int tx0, ty0;
+    tile_pixel(tile, tiles_x, 0, tx0, ty0);
     const bool inside = mpx < W && mpy < H;
     const uint2 range = ranges[tile];
     const int lane = threadIdx.x & 31;
@@ -692,7 +704,7 @@ __global__ void __launch_bounds__(256) k_render_backward(const uint2 *__restrict
             const bool act = threadIdx.x < n_active;
             const int pp = act ? st.list[threadIdx.x] : 0;
             int px, py;
-            tile_pixel(tile, tiles_x, pp, px, py);
+            tile_pixel_at(tx0, ty0, pp, px, py);
             const float fpx = (float)px, fpy = (float)py;
             const uint32_t plast = act ? st.last[pp] : 0u;
             const float Tfin = s_Tfin[pp];
