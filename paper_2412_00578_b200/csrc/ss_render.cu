@@ -232,6 +232,11 @@ __device__ __forceinline__ void tma_gather4(void *dst, const CUtensorMap *tm, ui
 }
 
 __device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ float ex2_approx(float x) {
     float e;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x));
@@ -383,10 +388,15 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
             // (their lists differ only by Gaussians with alpha = 0 everywhere in the tile).
             const int cnt = ((int)min((uint32_t)B, range.y - start) + 1) & ~1;
             const uint32_t base = start - range.x + 1;
+            // the pair's 5 float4 by 32-bit shared addresses stepped per pair (the generic
+            // pointer's window base was rematerialised every iteration at 40 registers)
+            // (the loop runs on the address alone; the list index kk only feeds n_contrib)
+            const uint32_t va0 = smem_u32(&s.v[0][0]);
+            const uint32_t vend = va0 + (uint32_t)(cnt >> 1) * (5 * 16);
+            uint32_t kk = base;  // list index (1-based) of the pair's even Gaussian
 #pragma unroll kRenderUnroll
-            for (int k = 0; k < cnt; k += 2) {
-                const float4 *v = s.v[k >> 1];
-                const float4 v0 = v[0], v1 = v[1], v2 = v[2];
+            for (uint32_t va = va0; va < vend; va += 5 * 16, kk += 2) {
+                const float4 v0 = lds128(va), v1 = lds128(va + 16), v2 = lds128(va + 32);
                 // q = (p - mu)^T Sigma^-1 (p - mu): dx = px - x, u = fma(a, dx, 2b dy),
                 // q = fma(dx, u, (c dy) dy)
                 const float2 dx = __fadd2_rn(FX, make_float2(v0.x, v0.y));
@@ -394,13 +404,13 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
                 const float2 u = __ffma2_rn(make_float2(v1.x, v1.y), dx, __fmul2_rn(make_float2(v1.z, v1.w), dy));
                 const float2 q = __ffma2_rn(dx, u, __fmul2_rn(__fmul2_rn(make_float2(v2.x, v2.y), dy), dy));
                 const float2 ql = __fmul2_rn(q, f2(-0.72134752044448170f));  // -q/2 in log2 units
-                const float4 v3 = v[3];
+                const float4 v3 = lds128(va + 48);
                 const float2 se = __fmul2_rn(make_float2(v3.x, v3.y), make_float2(ex2_approx(ql.x), ex2_approx(ql.y)));
                 const float2 al = make_float2(q.x <= v2.z ? fminf(0.99f, se.x) : 0.0f,   // alpha >= 1/255
                                               q.y <= v2.w ? fminf(0.99f, se.y) : 0.0f);  // (R15, R16)
                 const float2 om = __fadd2_rn(f2(1.0f), make_float2(-al.x, -al.y));
                 const float T1 = T * om.x, T2 = T1 * om.y;
-                const float4 v4 = v[4];
+                const float4 v4 = lds128(va + 64);
                 if (T2 < 1e-4f) {  // R16: a Gaussian of the pair terminates the pixel, before blending
                     if (T1 >= 1e-4f) {  // the even one still blends
                         const float w = al.x * T;
@@ -408,7 +418,7 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
                         C1 = fmaf(v3.w, w, C1);
                         C2 = fmaf(v4.z, w, C2);
                         T = T1;
-                        if (NC) last = al.x > 0.0f ? base + (uint32_t)k : last;
+                        if (NC) last = al.x > 0.0f ? kk : last;
                     }
                     done = true;
                     break;
@@ -418,7 +428,7 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
                 C1 = fmaf(v4.y, w.y, fmaf(v3.w, w.x, C1));
                 C2 = fmaf(v4.w, w.y, fmaf(v4.z, w.x, C2));
                 T = T2;
-                if (NC) last = al.y > 0.0f ? base + (uint32_t)(k + 1) : (al.x > 0.0f ? base + (uint32_t)k : last);
+                if (NC) last = al.y > 0.0f ? kk + 1 : (al.x > 0.0f ? kk : last);
             }
             st.T[pp] = T;
             st.C0[pp] = C0;
