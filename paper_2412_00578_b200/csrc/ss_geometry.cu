@@ -356,16 +356,17 @@ __global__ void __launch_bounds__(kPreThreads, kPre32Blocks) k_preprocess32(int 
     // warp chunks of 32 Gaussians: the first one static (global warp id), then tickets (the
     // next chunk fetched one step ahead, with its mean), so that the warps of the persistent
     // grid finish together (grid-stride: 0.157 ms single-stream, tickets: 0.144 ms)
+    // The ticket of the chunk after next is taken each step and consumed one step later, so
+    // the atomic's round trip is not on the path to the next mean's load.
     const int nwarps_all = (gridDim.x * blockDim.x) >> 5;
-    int c_next = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int c_next = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // chunk of the next step
+    uint32_t t_after = 0;  // lane 0: ticket of the step after (pending)
+    if (lane == 0) t_after = atomicAdd(ticket, 1u);
     int i = c_next * 32 + lane;
     float4 mo_next = i < n ? mean_opac[i] : make_float4(0.f, 0.f, -1.f, 0.f);
     for (int i0 = c_next * 32; i0 < n; i0 = c_next * 32, i = i0 + lane) {
-        {
-            uint32_t t = 0;
-            if (lane == 0) t = atomicAdd(ticket, 1u);
-            c_next = nwarps_all + (int)__shfl_sync(0xffffffffu, t, 0);
-        }
+        c_next = nwarps_all + (int)__shfl_sync(0xffffffffu, t_after, 0);
+        if (lane == 0) t_after = atomicAdd(ticket, 1u);
         const bool valid = i < n;
         const float4 mo = mo_next;
         const int in = c_next * 32 + lane;
