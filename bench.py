@@ -389,7 +389,7 @@ def run_ours(args):
     # has the GPU to itself there, so its share of the frame matches the ncu launch list); the
     # longer one is the line's roofline.  `traffic` = its DRAM bytes per launch from the
     # committed ncu --set full summary (profiles/traffic.json), when present.
-    traffic = {}
+    traffic, winst = {}, {}
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     tsrc = None
     if os.path.exists(tpath):
@@ -400,6 +400,8 @@ def run_ours(args):
             for kn in ("k_preprocess", "k_render<"):
                 if k.startswith(kn):
                     traffic[kn.rstrip("<")] = traffic.get(kn.rstrip("<"), 0.0) + v["dram_bytes"]
+                    if v.get("warp_inst"):
+                        winst[kn.rstrip("<")] = winst.get(kn.rstrip("<"), 0.0) + v["warp_inst"]
     pre = stage_info["preprocess"]
     kern = {
         "k_preprocess": {"bound": "hbm", "launch_ms": pre_iso_ms,
@@ -421,6 +423,18 @@ def run_ours(args):
                         "unit_work": "18 FP32 ops per (pixel, Gaussian) evaluation x E_pix (SURVEY §8(d)); "
                                      "E_pix from ss_render_stats",
                         "peak_source": f"derived: 148 SM x {FP32_LANES_PER_SM} FP32 lanes x 2 flop x {sm_max:.0f} MHz"}
+    # The render's instruction-issue view: the FP32 roofline counts only the method's 18 flop
+    # per evaluation, while the loop also issues its shared-memory loads, selects, the SFU
+    # exponential and the termination test; the issue ceiling (4 warp instructions per SM per
+    # cycle) bounds the kernel whatever the mix.  Warp instructions per launch from the same
+    # committed capture as `traffic`, over the live launch time.
+    if winst.get("k_render"):
+        issue_peak = 148 * 4 * sm_max * 1e6
+        kern["k_render"]["issue"] = {
+            "warp_inst_per_launch": winst["k_render"], "achieved": winst["k_render"] / (r_ms / 1e3),
+            "peak": issue_peak, "unit": "warp inst/s", "frac": winst["k_render"] / (r_ms / 1e3) / issue_peak,
+            "peak_source": f"148 SM x 4 schedulers x 1 warp instruction per cycle x {sm_max:.0f} MHz",
+            "source": tsrc}
     dom = max(kern, key=lambda k: kern[k]["launch_ms"])
     d = kern[dom]
     roof = {"bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"], "unit": d["unit"], "frac": d["frac"],

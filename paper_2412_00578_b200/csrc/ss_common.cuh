@@ -31,7 +31,10 @@ constexpr int kSortThreads = 256;
 constexpr int kSortItems = SS_SORT_ITEMS;
 constexpr int kSortTile = kSortThreads * kSortItems;   // 3072 keys per block tile
 constexpr int kInlineEnt = 6;                          // super-tile entries stored in the emission record
-constexpr int kLaneRows = 6;                           // AccuTile lines a preprocess lane sweeps alone
+#ifndef SS_LANE_ROWS
+#define SS_LANE_ROWS 6
+#endif
+constexpr int kLaneRows = SS_LANE_ROWS;                 // AccuTile lines a preprocess lane sweeps alone
 constexpr int kDepthPasses = 4;                        // 32-bit depth keys, 8-bit digits
 constexpr uint32_t kInfoEntInline = 0x100u;            // erec info: entries stored in the record
 constexpr uint32_t kInfoCols = 0x200u;                 // erec info: columns sweep (lines are tile columns)

@@ -64,14 +64,17 @@ def traffic(*paths):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         ir, iw, it = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum"), \
             hdr.index("gpu__time_duration.sum")
+        ii = hdr.index("smsp__inst_executed.sum") if "smsp__inst_executed.sum" in hdr else None
         for r in rows[2:]:
             name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "").replace("unnamed>::", "")
             b = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
             us = float(r[it]) * (1e-3 if units[it] == "nsecond" else 1.0)
-            agg[name].append((b, us))
+            wi = float(r[ii]) if ii is not None and r[ii] else 0.0
+            agg[name].append((b, us, wi))
     src = ", ".join(os.path.basename(p) for p in paths)
     print(json.dumps({"source": f"ncu --set full ({src}): dram__bytes_read.sum + dram__bytes_write.sum per launch",
-                      "kernels": {k: {"dram_bytes": sum(b for b, _ in v) / len(v), "us": sum(u for _, u in v) / len(v),
+                      "kernels": {k: {"dram_bytes": sum(x[0] for x in v) / len(v), "us": sum(x[1] for x in v) / len(v),
+                                      "warp_inst": sum(x[2] for x in v) / len(v),
                                       "captures": len(v)} for k, v in agg.items()}}, indent=1))
 
 
