@@ -374,7 +374,10 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
             int px, py;
             tile_pixel_at(tx0, ty0, p0 + pp, px, py);
             const float2 FX = f2((float)px), FY = f2((float)py);
-            float T = st.T[pp], C0 = st.C0[pp], C1 = st.C1[pp], C2 = st.C2[pp];
+            // colour sums: (r, g) as one f32x2 (each lane the channel's own sequential FMA chain),
+            // b scalar
+            float T = st.T[pp], C2 = st.C2[pp];
+            float2 C01 = make_float2(st.C0[pp], st.C1[pp]);
             uint32_t last = st.last[pp];
             bool done = false;
             // pairs of consecutive Gaussians over the padded batch (padding slots never
@@ -414,8 +417,7 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
                 if (T2 < 1e-4f) {  // R16: a Gaussian of the pair terminates the pixel, before blending
                     if (T1 >= 1e-4f) {  // the even one still blends
                         const float w = al.x * T;
-                        C0 = fmaf(v3.z, w, C0);
-                        C1 = fmaf(v3.w, w, C1);
+                        C01 = __ffma2_rn(make_float2(v3.z, v3.w), f2(w), C01);
                         C2 = fmaf(v4.z, w, C2);
                         T = T1;
                         if (NC) last = al.x > 0.0f ? kk : last;
@@ -424,15 +426,14 @@ __global__ void __launch_bounds__(PIX, SS_RENDER_MINB * 256 / PIX) k_render(cons
                     break;
                 }
                 const float2 w = __fmul2_rn(al, make_float2(T, T1));
-                C0 = fmaf(v4.x, w.y, fmaf(v3.z, w.x, C0));
-                C1 = fmaf(v4.y, w.y, fmaf(v3.w, w.x, C1));
+                C01 = __ffma2_rn(make_float2(v4.x, v4.y), f2(w.y), __ffma2_rn(make_float2(v3.z, v3.w), f2(w.x), C01));
                 C2 = fmaf(v4.w, w.y, fmaf(v4.z, w.x, C2));
                 T = T2;
                 if (NC) last = al.y > 0.0f ? kk + 1 : (al.x > 0.0f ? kk : last);
             }
             st.T[pp] = T;
-            st.C0[pp] = C0;
-            st.C1[pp] = C1;
+            st.C0[pp] = C01.x;
+            st.C1[pp] = C01.y;
             st.C2[pp] = C2;
             if (NC) st.last[pp] = last;
             my_pp = (uint32_t)pp;
