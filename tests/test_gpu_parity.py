@@ -224,3 +224,14 @@ def test_knife_edge_tile_decisions(mode, seed):
     assert np.array_equal(rz.sorted_keys().cpu().numpy().view(np.uint64)[:f.P], f.keys)
     assert np.array_equal(rz.ranges().cpu().numpy().view(np.uint32), f.ranges)
     assert t["deferred"] > 0, "the float64 fallback was not exercised"
+
+
+def test_maximum_image_size():
+    """At the limits include/ss.h states: a 4096 x 4096 view is 256 x 256 = 65,536 tiles (the
+    tile maximum, 256 per axis) and 64 x 64 = 4,096 super-tiles (the level-1 maximum).  150k
+    Gaussians of the MNR360 recipe: records, counts, sorted keys, ranges bit-exact and the whole
+    image within 1e-4 of the oracle (the full _check_frame battery)."""
+    scene, _ = synth.make_workload("mnr360-3m", n=150000)
+    cam = synth.orbit_cameras(1, 4096, 4096)[0]
+    assert cam.tiles_x * cam.tiles_y == 65536
+    _check_frame(scene, cam, "accutile", bg=(0.1, 0.2, 0.3))
