@@ -163,14 +163,16 @@ __device__ __forceinline__ void span_entries(uint2 *__restrict__ stg, uint32_t g
 #pragma unroll 1
         for (int C = lo >> 2; C <= (hi - 1) >> 2; ++C) {
             uint32_t mask = 0;
+            const int c4 = 4 * C;
 #pragma unroll 1
             for (int s = q; s < q2; ++s) {
-                const int a = max((int)(v[s] & 0x1FFu), 4 * C), b = min((int)((v[s] >> 9) & 0x1FFu), 4 * C + 4);
-                if (b > a) {
-                    const uint32_t bits = ((1u << (b - a)) - 1u) << (a - 4 * C);
-                    const int r = (int)(v[s] >> 18) & 3;
-                    mask |= cols ? (spread4(bits) << r) : (bits << (4 * r));
-                }
+                // the span's tiles in columns 4C .. 4C+3 as a nibble, branch-free (0 if disjoint):
+                // bits max(lo, 4C) - 4C .. min(hi, 4C + 4) - 4C - 1
+                const int a = min(max((int)(v[s] & 0x1FFu) - c4, 0), 4);
+                const int b = min(max(c4 + 4 - (int)((v[s] >> 9) & 0x1FFu), 0), 4);
+                const uint32_t bits = (0xFu << a) & (0xFu >> b) & 0xFu;
+                const int r = (int)(v[s] >> 18) & 3;
+                mask |= cols ? (spread4(bits) << r) : (bits << (4 * r));
             }
             put_entry(stg, e++, cols ? (uint32_t)(C * stx + band) : (uint32_t)(band * stx + C), g, mask);
         }
