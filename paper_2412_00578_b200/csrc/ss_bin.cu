@@ -564,7 +564,15 @@ __device__ __forceinline__ uint32_t l2_load(const uint2 *__restrict__ ent, uint3
     return n;
 }
 
-// Pairs per tile in each level-2 block (16 ballots per 32 entries) -> BC[blk][16].
+// 8 mask bits -> bit t at position 4 t (nibble fields).
+__device__ __forceinline__ uint32_t spread8_nibbles(uint32_t x) {
+    x = (x | (x << 12)) & 0x000F000Fu;
+    x = (x | (x << 6)) & 0x03030303u;
+    return (x | (x << 3)) & 0x11111111u;
+}
+
+// Pairs per tile in each level-2 block (per-thread nibble counters, 16 warp reductions) ->
+// BC[blk][16].
 __global__ void __launch_bounds__(kL2Threads) k_l2_count(const uint32_t *__restrict__ overflow, int stx,
                                                          int tiles_x, int tiles_y, int n_super,
                                                          const uint32_t *__restrict__ st_total,
@@ -583,14 +591,21 @@ __global__ void __launch_bounds__(kL2Threads) k_l2_count(const uint32_t *__restr
         const uint32_t n = min((uint32_t)kL2Block, st_total[bl.x] - bl.y);
         uint2 v[kL2PerThread];
         l2_load(ent, st_base[bl.x] + bl.y, n, v);
-        uint32_t cnt = 0;
+        // per-thread counts of the 16 tiles as 4-bit fields (bit t of a mask -> field t; at most
+        // kL2PerThread = 8 per field), then one warp reduction per tile
+        uint32_t a0 = 0, a1 = 0;  // tiles 0-7, 8-15
 #pragma unroll
         for (int q = 0; q < kL2PerThread; ++q) {
+            a0 += spread8_nibbles(v[q].y & 0xFFu);
+            a1 += spread8_nibbles((v[q].y >> 8) & 0xFFu);
+        }
+        static_assert(kL2PerThread <= 15, "4-bit per-thread tile counters");
+        uint32_t cnt = 0;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) {
-                const uint32_t bal = __ballot_sync(0xffffffffu, (v[q].y >> t) & 1u);
-                if (lane == t) cnt += __popc(bal);
-            }
+        for (int t = 0; t < 16; ++t) {
+            const uint32_t c = ((t < 8 ? a0 : a1) >> (4 * (t & 7))) & 0xFu;
+            const uint32_t sum = __reduce_add_sync(0xffffffffu, c);
+            if (lane == t) cnt = sum;
         }
         if (lane < 16) s_cnt[w][lane] = cnt;
         __syncthreads();
