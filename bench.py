@@ -699,9 +699,10 @@ def run_ours(args):
                                       "of the tile (AccuTile tests the continuous cell, DESIGN.md R23)"},
             "stages_timing": "single-stream pass of V frames after the timed region (every stage bracketed by events)",
             "roofline": roof,
-            # ours per frame: k_preprocess, 4 x k_onesweep, k_escan_reduce, k_escan_apply, k_entries,
-            # k_big_entries, k_l1_count, k_l1_scan, k_l1_emit, k_l2_count, k_l2_scan, k_l2_write, k_render
-            "gpu_launches": n_timed * 16,
+            # ours per frame (profiles/r02/r02_v10_launches.txt): k_preprocess32, k_preprocess64 (the
+            # deferred queue), 4 x k_onesweep, k_escan_reduce, k_escan_apply, k_entries, k_big_entries,
+            # k_l1_count, k_l1_scan, k_l1_emit, k_l2_count, k_l2_scan, k_l2_write, k_render
+            "gpu_launches": n_timed * 17,
             "clocks": clk,
             "e2e": e2e,
             "prune_score": score_info,
