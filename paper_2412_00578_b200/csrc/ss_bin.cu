@@ -354,7 +354,6 @@ __global__ void __launch_bounds__(kBinWarps * 32, 3) k_l1_count(const uint32_t *
     const uint32_t E = *total_entries, c = blockIdx.x;
     if (*overflow || c * (uint32_t)kEntChunk >= E) return;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t lt_mask = (1u << lane) - 1u;
     for (int s = threadIdx.x; s < kBinWarps * n_super; s += blockDim.x) hist[s] = 0;
     uint32_t b, B0, B1;
     unit_bounds(c, w, E, b, B0, B1);
@@ -371,7 +370,6 @@ __global__ void __launch_bounds__(kBinWarps * 32, 3) k_l1_count(const uint32_t *
     // counts only (no ranks): one shared-memory atomic per entry (the entries of a warp are in
     // depth order, so their super-tiles rarely coincide); ballot-ranked aggregation as in
     // k_l1_emit measured 10 us slower per frame
-    (void)lt_mask;
 #pragma unroll
     for (int q = 0; q < kPerLane; ++q)
         if ((uint32_t)q * 32 + lane < n) atomicAdd(&h[st[q]], 1u);
