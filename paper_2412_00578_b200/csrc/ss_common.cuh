@@ -42,7 +42,10 @@ constexpr uint32_t kInfoAccuTile = 0x400u;             // erec info: tile set of
 constexpr uint32_t kInfoSpanInline = 0x800u;           // erec info: line spans stored in the record
 constexpr int kInfoEntShift = 12;                      // erec info bits 12..31: super-tile entries
 constexpr int kSuperTile = 4;                          // super-tile side in tiles (ss_tilegeom.cuh)
-constexpr int kEntWarp = 512;                          // entries per warp unit of level 1
+#ifndef SS_ENT_WARP
+#define SS_ENT_WARP 512
+#endif
+constexpr int kEntWarp = SS_ENT_WARP;                  // entries per warp unit of level 1
 constexpr int kBinWarps = 8;                           // warps per level-1 CTA
 constexpr int kEntChunk = kEntWarp * kBinWarps;        // entries per level-1 chunk (CTA)
 constexpr int kL2BlockEntries = 2048;                  // entries per level-2 block (CTA)
