@@ -197,6 +197,44 @@ def knife_scene(n=20000, seed=11, sh_degree=0) -> tuple[Scene, Camera]:
     return scene, cam
 
 
+def tangent_scene(n=20000, seed=21, sh_degree=0) -> tuple[Scene, Camera]:
+    """Stress scene for the swept-axis extremes (the float32-certified geometry's near-tangent
+    lines, R28): Gaussians flat along the optical axis and rotated about it by 0 or a
+    small-to-moderate angle, placed so that an extreme of their SnugBox, mu_y -+ h_y (or
+    mu_x -+ h_x), lands on or within 1e-5..1e-1 px of a tile line -- the Algorithm-1 boundary
+    line next to the extreme then grazes the ellipse (discriminant near 0).  h is the
+    closed-form half-extent sqrt(t Sigma_2D) of the camera's projection near the image centre
+    (the exact float32 value differs slightly, which spreads the distances further)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    W = H = 256
+    cam = look_at((0, 0, 0), (0, 0, 1), W, H, 60.0, up=(0, -1, 0))
+    f = cam.fx
+    z = rng.uniform(2.0, 8.0, n)
+    sx_px = np.exp(rng.uniform(math.log(0.5), math.log(60.0), n))
+    sy_px = sx_px * np.exp(rng.uniform(math.log(0.05), math.log(20.0), n))
+    theta = np.where(rng.uniform(size=n) < 0.3, 0.0, rng.uniform(-0.6, 0.6, n))
+    opac = rng.uniform(0.02, 0.999, n)
+    t = 2.0 * np.log(255.0 * opac)
+    c2, s2 = np.cos(theta) ** 2, np.sin(theta) ** 2
+    sxx = c2 * sx_px ** 2 + s2 * sy_px ** 2 + 0.3
+    syy = s2 * sx_px ** 2 + c2 * sy_px ** 2 + 0.3
+    hx, hy = np.sqrt(t * sxx), np.sqrt(t * syy)
+    delta = rng.choice([0.0, 1e-5, -1e-5, 1e-3, -1e-3, 0.1, -0.1], n) * rng.uniform(0.5, 1.5, n)
+    line = 16.0 * rng.integers(1, 16, n)
+    side = np.where(rng.uniform(size=n) < 0.5, -1.0, 1.0)
+    on_y = rng.uniform(size=n) < 0.5
+    u = np.where(on_y, rng.uniform(16, 240, n), line - side * hx + delta)
+    v = np.where(on_y, line - side * hy + delta, rng.uniform(16, 240, n))
+    x = (u - cam.cx) * z / f
+    y = (v - cam.cy) * z / f
+    scale = np.stack([sx_px * z / f, sy_px * z / f, np.full(n, 1e-4) * z / f], 1)
+    quat = np.stack([np.cos(theta / 2), np.zeros(n), np.zeros(n), np.sin(theta / 2)], 1)
+    mean_opac = np.stack([x, y, z, opac], 1).astype(np.float32)
+    sc = np.concatenate([scale, np.zeros((n, 1))], 1).astype(np.float32)
+    scene = Scene(mean_opac, sc, quat.astype(np.float32), _sh_planes(rng, n, sh_degree), sh_degree, "tangent")
+    return scene, cam
+
+
 def dense_scene(n=12000, seed=5, tie_frac=0.5, sh_degree=1) -> tuple[Scene, Camera]:
     """Tile-sort stress case on the tiny camera: means packed into a 64x64 px window at the
     image centre, so the central tiles' lists are longer than one shared-memory sort

@@ -205,14 +205,17 @@ def test_phantom_pairs_invariant(name):
 
 
 @pytest.mark.parametrize("mode", ["snugbox", "accutile"])
-@pytest.mark.parametrize("seed", [11, 12, 13])
+@pytest.mark.parametrize("seed", [11, 12, 13, "tangent-21", "tangent-22"])
 def test_knife_edge_tile_decisions(mode, seed):
     """synth.knife_scene: means on / within 1e-5 px of tile lines, axis ratios up to 1e3,
     t ~ 0 and near-1 opacities, clipped giants.  Every count, sorted key and range equals the
     oracle's float64 tile sets bit-exactly; the float32-certified path must have handed some
     Gaussians to the float64 fallback here (pre_deferred > 0), so both paths are exercised."""
     from paper_2412_00578_b200.raster import DeviceScene, Rasterizer
-    scene, cam = synth.knife_scene(seed=seed)
+    if isinstance(seed, str):  # swept-axis extremes on tile lines (near-tangent Algorithm-1 lines)
+        scene, cam = synth.tangent_scene(seed=int(seed.split("-")[1]))
+    else:
+        scene, cam = synth.knife_scene(seed=seed)
     rz = Rasterizer(DeviceScene.from_host(scene), cam.width, cam.height, mode=mode)
     rz.ensure_capacity(cam)
     rz.render_frame(cam)
