@@ -238,3 +238,28 @@ def test_maximum_image_size():
     cam = synth.orbit_cameras(1, 4096, 4096)[0]
     assert cam.tiles_x * cam.tiles_y == 65536
     _check_frame(scene, cam, "accutile", bg=(0.1, 0.2, 0.3))
+
+
+@pytest.mark.parametrize("name", ["tiny", "tiny-lowsigma", "orbit", "dense"])
+def test_plain_and_ncontrib_forward_equal(name):
+    """The plain forward (the bench's frame path) and the n_contrib forward (the score's first
+    walk) are separate instantiations of k_render; their images and T must be bitwise equal.  (It
+    also guarded the batch-level culling experiment of NEXT-4: culled vs not.)"""
+    from paper_2412_00578_b200.raster import DeviceScene, Rasterizer
+    if name == "orbit":
+        scene, cams = synth.orbit_scene(30000, 5), synth.orbit_cameras(3, 200, 136)
+    elif name == "dense":
+        scene, cam = synth.dense_scene()
+        cams = [cam]
+    else:
+        scene, cams = synth.make_workload(name)
+    ds = DeviceScene.from_host(scene)
+    for cam in cams:
+        rz = Rasterizer(ds, cam.width, cam.height)
+        rz.ensure_capacity(cam)
+        bg = (0.1, 0.3, 0.2)
+        img_c, T_c, _ = rz.render_frame(cam, bg, want_T=True)
+        img_c, T_c = img_c.clone(), T_c.clone()
+        img_n, T_n, _ = rz.render_frame(cam, bg, want_T=True, want_ncontrib=True)
+        torch.cuda.synchronize()
+        assert torch.equal(img_c, img_n) and torch.equal(T_c, T_n)
