@@ -53,8 +53,8 @@ def _pipeline(scene, cams, views, mode):
     return ds, pipe
 
 
-def _check_views(name, views, mode, bg=(0.0, 0.0, 0.0), score=False):
-    scene, cams = synth.make_workload(name)
+def _check_views(name, views, mode, bg=(0.0, 0.0, 0.0), score=False, scene_cams=None):
+    scene, cams = scene_cams if scene_cams is not None else synth.make_workload(name)
     _W[name] = (scene, cams)
     ds, pipe = _pipeline(scene, cams, views, mode)
     assert len(views) <= pipe.n_streams  # one view per workspace: every intermediate stays inspectable
@@ -120,3 +120,25 @@ def test_playroom_score_views():
 def test_garden_accutile():
     """Mip-NeRF 360 garden-shaped (5.8M, 1297x840)."""
     _check_views("garden", [40, 133], "accutile")
+
+
+def test_mnr360_pruned_regime():
+    """BASELINE config 5 at full size: U~ of the 3.0M-Gaussian MNR360 scene over all 185 views
+    (FramePipeline.score_views, float64), the prune step removing 90% (raster.prune, ties by
+    index), then four views of the surviving 300k Gaussians through the bench's timed path:
+    every count, key, range and pixel vs the oracle run on the same surviving set (the host
+    scene's subset by the GPU keep mask, in the compaction's stable order)."""
+    from paper_2412_00578_b200.raster import DeviceScene, FramePipeline, prune
+    scene, cams = synth.make_workload("mnr360-3m")
+    ds = DeviceScene.from_host(scene)
+    sp = FramePipeline(ds, cams[0].width, cams[0].height, n_streams=4)
+    sp.ensure_capacity(cams)
+    sc = torch.zeros(ds.n, dtype=torch.float64, device="cuda")
+    sp.score_views(cams, sc)
+    _, keep = prune(ds, sc, 0.9)
+    torch.cuda.synchronize()
+    idx = np.nonzero(keep.cpu().numpy())[0]
+    assert len(idx) == scene.n - int(0.9 * scene.n)
+    del sp, ds
+    r = _check_views("mnr360-3m-pruned", [0, 46, 92, 138], "accutile", scene_cams=(scene.subset(idx), cams))
+    assert r["values_checked"] == 4 * 3 * 1297 * 840
