@@ -126,8 +126,9 @@ def test_mnr360_pruned_regime():
     """BASELINE config 5 at full size: U~ of the 3.0M-Gaussian MNR360 scene over all 185 views
     (FramePipeline.score_views, float64), the prune step removing 90% (raster.prune, ties by
     index), then four views of the surviving 300k Gaussians through the bench's timed path:
-    every count, key, range and pixel vs the oracle run on the same surviving set (the host
-    scene's subset by the GPU keep mask, in the compaction's stable order)."""
+    every count, key, range and pixel, and the whole score vector of those views (with a
+    background), vs the oracle run on the same surviving set (the host scene's subset by the GPU
+    keep mask, in the compaction's stable order)."""
     from paper_2412_00578_b200.raster import DeviceScene, FramePipeline, prune
     scene, cams = synth.make_workload("mnr360-3m")
     ds = DeviceScene.from_host(scene)
@@ -140,5 +141,6 @@ def test_mnr360_pruned_regime():
     idx = np.nonzero(keep.cpu().numpy())[0]
     assert len(idx) == scene.n - int(0.9 * scene.n)
     del sp, ds
-    r = _check_views("mnr360-3m-pruned", [0, 46, 92, 138], "accutile", scene_cams=(scene.subset(idx), cams))
-    assert r["values_checked"] == 4 * 3 * 1297 * 840
+    r = _check_views("mnr360-3m-pruned", [0, 46, 92, 138], "accutile", bg=(0.2, 0.1, 0.0), score=True,
+                     scene_cams=(scene.subset(idx), cams))
+    assert r["values_checked"] == 4 * 3 * 1297 * 840 and r["score_checked"] > 1000, r
