@@ -91,6 +91,8 @@ WORKLOADS = {
     "tiny": Workload("tiny", 1000, 256, 256, 1, 0, "tiny"),
     "tiny-lowsigma": Workload("tiny-lowsigma", 1000, 256, 256, 1, 0, "tiny", extra={"low_sigma": True}),
     "tiny-deg0": Workload("tiny-deg0", 1000, 256, 256, 1, 0, "tiny", extra={"sh_degree": 0}),
+    "tiny-deg1": Workload("tiny-deg1", 1000, 256, 256, 1, 0, "tiny", extra={"sh_degree": 1}),
+    "tiny-deg2": Workload("tiny-deg2", 1000, 256, 256, 1, 0, "tiny", extra={"sh_degree": 2}),
     "truck": Workload("truck", 2_500_000, 979, 546, 251, 1, "orbit"),
     "garden": Workload("garden", 5_800_000, 1297, 840, 185, 2, "orbit"),
     "playroom": Workload("playroom", 2_300_000, 1264, 832, 225, 3, "room", fovx_deg=65.0),

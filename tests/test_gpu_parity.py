@@ -103,7 +103,7 @@ def _check_frame(scene, cam, mode, bg=(0.0, 0.0, 0.0), capacity=None, image=True
 
 
 @pytest.mark.parametrize("mode", MODES)
-@pytest.mark.parametrize("name", ["tiny", "tiny-lowsigma", "tiny-deg0"])
+@pytest.mark.parametrize("name", ["tiny", "tiny-lowsigma", "tiny-deg0", "tiny-deg1", "tiny-deg2"])
 def test_tiny_parity(name, mode):
     scene, cams = synth.make_workload(name)
     _check_frame(scene, cams[0], mode)
