@@ -47,6 +47,22 @@ def enqueue(stage, j, cam, st):
 
 
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+if os.environ.get("SS_L2_PERSIST"):  # experiment: keep the scene's means (read by every frame) in L2
+    from cuda.bindings import runtime as rt
+    nbytes = int(ds.mean_opac.numel() * 4)
+    frac = float(os.environ.get("SS_L2_PERSIST"))
+    rt.cudaDeviceSetLimit(rt.cudaLimit.cudaLimitPersistingL2CacheSize, nbytes)
+    for st in pipe.streams:
+        v = rt.cudaStreamAttrValue()
+        w = v.accessPolicyWindow
+        w.base_ptr = ds.mean_opac.data_ptr()
+        w.num_bytes = nbytes
+        w.hitRatio = frac
+        w.hitProp = rt.cudaAccessProperty.cudaAccessPropertyPersisting
+        w.missProp = rt.cudaAccessProperty.cudaAccessPropertyStreaming
+        v.accessPolicyWindow = w
+        err = rt.cudaStreamSetAttribute(st.cuda_stream, rt.cudaStreamAttributeAccessPolicyWindow, v)
+        print("policy", err, file=sys.stderr)
 res = {}
 for stage, name in ((1, "a1"), (2, "a1-a2"), (3, "a1-a5"), (4, "a1-a6")):
     graphs = {}
